@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: post-rollout tokens/s (advantage + loss + reshard) on B200, BASELINE.json's metric.
+
+One step = the post-rollout DAG slice of the GRPO preset (distflow/dag.hpp:341-354) over one synthetic batch
+already resident in HBM:
+  group_advantage_compute (dp_p = 8 logical workers)  -> reshard dp 8 -> dp 4 (tp 2)  -> actor_train loss (dp 4)
+    * GRPO group advantage, f64 per rollout (dfx_grpo_advantage)
+    * DataBuffer reshard, box placement (B = 1 store, W = 8 logical workers over the N GPUs);
+      at N <= 4 every consumer group's records are already on its GPU -> zero-copy views, no bytes move;
+      at N = 8 TP partners exchange their groups over NVLink (NCCL)
+    * fused per-token advantage broadcast + PPO clipped surrogate + k3 KL + token-mean, one loss group per
+      consumer DP group (dfx_ppo_loss, the dominant kernel)
+Workload per GPU: C2 = 1024 prompts x n=16 x UNIFORM[1,4096] tokens (~33.5M tokens, 571 MB of streams; larger
+than L2, so no flush is needed between steps). Weak scaling: every rank holds its own C2 batch.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: fn_group_advantage + BufferStore
+put/redistribute/get, compiled from /root/reference) plus the oracle's loss port (the reference has no loss) on a
+bounded sample, on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "post-rollout tokens/s (adv+loss+reshard) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "tokens/s"
+C2 = dict(records=1024, n_roll=16, dist=("uniform", 0, 1, 4096), seed=1)
+BYTES_PER_TOKEN = 17      # lp, old_lp, ref_lp (3x4) + mask (1) + advantage write (4)
+BYTES_PER_ROLLOUT = 16    # f64 advantage read + i64 cu_seqlens read
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="dfx", choices=["dfx", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--records", type=int, default=C2["records"])
+    return ap.parse_args()
+
+
+# ---- clocks (NVML, sampled during the timed region) -----------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for bit, name in self.REASONS.items():
+            if r & bit and bit != 0x1:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+            time.sleep(self._period)
+
+    def __enter__(self):
+        if self._nv:
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._nv:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_loss_slots.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ---- the GPU arm ------------------------------------------------------------------------------------
+def run_dfx(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_13833_b200 as dfx
+    from paper_2507_13833_b200 import _abi
+    from paper_2507_13833_b200.packed import _ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2507_13833_b200.reshard import BoxReshard
+
+    L = _abi.lib()
+    R, n = args.records, C2["n_roll"]
+    distrib = dfx.TokenDist(*C2["dist"])
+    batch = dfx.PackedBatch.synthetic(C2["seed"], R, n, distrib, device=dev, first_id=rank * R)
+    torch.cuda.synchronize()
+    tokens_local = batch.token_span
+    ctx = dfx.StageContext()
+    ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
+    stream = torch.cuda.current_stream(dev)
+    resh = BoxReshard(world, rank, dev, producer_dp=8, consumer_dp=4)
+
+    ev0, ev1 = C.c_void_p(), C.c_void_p()
+    _abi.check(L.dfx_event_create(C.byref(ev0)))
+    _abi.check(L.dfx_event_create(C.byref(ev1)))
+    kern_ms = []
+
+    def step(time_kernel=False):
+        dfx.fn_group_advantage(dfx.NodeSpec("group_advantage_compute"), batch, ctx)
+        consumer, lgo = resh.exchange(batch, ctx)
+        res = dfx.ppo_loss(consumer, ctx, adv_source="rollout", loss_group_off=lgo, adv_tok_out=True,
+                           events=(ev0, ev1) if time_kernel else None)
+        if time_kernel:
+            ms = C.c_float()
+            _abi.check(L.dfx_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+            kern_ms.append(ms.value)
+        return res, consumer
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # kernel-level timing of the dominant kernel (events on its own stream, separate pass)
+    for _ in range(min(args.steps, 50)):
+        step(time_kernel=True)
+    torch.cuda.synchronize()
+
+    # the steady-state step is launch-bound at this size: capture it once in a CUDA graph when the
+    # reshard has no host synchronization (all N <= 4 box placements)
+    graph = None
+    if resh.local and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for _ in range(args.steps):
+            run()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_step = s0.elapsed_time(s1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        tt = torch.tensor([float(tokens_local)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt)
+        tokens_total = float(tt.item())
+    else:
+        tokens_total = float(tokens_local)
+    value = tokens_total / (ms_step / 1e3)
+
+    # ---- e2e: same step through the public API from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, dfx, batch, ctx, resh, dev, stream, world)
+
+    # ---- roofline of the dominant kernel ----
+    kern = statistics.median(kern_ms) if kern_ms else None
+    bytes_launch = tokens_local * BYTES_PER_TOKEN + batch.n_rollouts * BYTES_PER_ROLLOUT
+    peak, peak_src = measured_peak_hbm()
+    roof = None
+    if kern:
+        ach = bytes_launch / (kern / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": ncu_traffic(), "kernel": "dfx::loss_slots_kernel", "kernel_ms": round(kern, 5),
+                "bytes_per_launch": bytes_launch, "peak_source": peak_src}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(R)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 group stats/accumulators)",
+            "data": "synthetic (keyed SplitMix64, generated on device; SURVEY.md §8(d))",
+            "config": {"workload": f"C2 per GPU: {R} prompts x n={n} x UNIFORM[1,4096] tokens "
+                                   f"(~{tokens_local/1e6:.1f}M tokens/GPU), GRPO adv -> reshard dp8->dp4(tp2) "
+                                   f"box placement B=1 W=8 -> clipped loss + k3 KL token-mean",
+                       "tokens_per_gpu": tokens_local, "global_tokens": int(tokens_total),
+                       "reshard": resh.describe(), "l2": "inputs (571 MB/GPU) larger than the 126 MB L2; no flush",
+                       "parallelism": f"dp{world} (logical dp8->dp4 over {world} GPU)",
+                       "cuda_graph": graph is not None},
+            "e2e": e2e, "gpu_launches": resh.launches_per_step + 3, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.result(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, dfx, batch, ctx, resh, dev, stream, world):
+    """Public-API step with host buffers: pinned host -> H2D of every input array, the step, D2H of the results."""
+    import torch
+
+    h = {}
+    d = {}
+    for name, t in [("ids", batch.ids), ("group_off", batch.group_off), ("roll_group", batch.roll_group),
+                    ("cu_seqlens", batch.cu_seqlens), ("reward", batch.channels["reward"])] + \
+            [(k, batch.streams[k]) for k in ("lp", "old_lp", "ref_lp", "mask")]:
+        h[name] = t.cpu().pin_memory()
+        d[name] = torch.empty_like(t)
+    eb = dfx.PackedBatch(batch.n_records, batch.n_rollouts, batch.token_base, batch.token_span, d["ids"],
+                         d["group_off"], d["roll_group"], d["cu_seqlens"], {"reward": d["reward"]},
+                         {k: d[k] for k in ("lp", "old_lp", "ref_lp", "mask")},
+                         host_group_off=batch.host_group_off, host_cu=batch.host_cu)
+    h2d = sum(v.numel() * v.element_size() for v in h.values())
+    n_groups = 4
+    out_h = torch.empty(n_groups * 7, dtype=torch.float64).pin_memory()
+    adv_h = torch.empty(batch.n_rollouts, dtype=torch.float64).pin_memory()
+    d2h = out_h.numel() * 8 + adv_h.numel() * 8
+
+    def e2e_step():
+        for k in h:
+            d[k].copy_(h[k], non_blocking=True)
+        dfx.fn_group_advantage(dfx.NodeSpec("group_advantage_compute"), eb, ctx)
+        consumer, lgo = resh.exchange(eb, ctx)
+        res = dfx.ppo_loss(consumer, ctx, adv_source="rollout", loss_group_off=lgo, adv_tok_out=True)
+        out_h.copy_(res["out"].reshape(-1), non_blocking=True)
+        adv_h.copy_(eb.channels["advantage"], non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 20))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(steps):
+        e2e_step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tokens = batch.token_span * world
+    return {"value": round(tokens / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 4), "steps": steps,
+            "path": "PackedBatch host->device copies + fn_group_advantage + BufferStore reshard + ppo_loss + "
+                    "D2H of loss/advantage"}
+
+
+# ---- CPU arm: the reference's own code (oracle/_ref) + the oracle loss port -------------------
+CPU_SAMPLE_RECORDS = 64
+
+
+def cpu_sample():
+    from oracle import oracle as O
+    sb = O.SynthBatch(C2["seed"], CPU_SAMPLE_RECORDS, C2["n_roll"], O.token_dist("uniform", 0, 1, 4096),
+                      streams=("lp", "old_lp", "ref_lp", "mask", "token_id"))
+    return O, sb
+
+
+def cpu_step(O, sb, nthreads):
+    """Reference fn_group_advantage + BufferStore reshard (dp8 -> dp4 tp2, B=1 W=8, one thread per worker)
+    on records whose payload is the 16 B/token streams (token id, lp, old, ref), then the loss port."""
+    T = sb.n_tokens
+    streams = [sb.token_id[:T], sb.lp[:T], sb.old_lp[:T], sb.ref_lp[:T]]
+    t0 = time.perf_counter()
+    adv_s, rs_s = O.ref_bench(sb, streams, 1, 8, 8, 1, 4, 2, nthreads, 1)
+    t1 = time.perf_counter()
+    adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    adv_tok = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
+    t2 = time.perf_counter()
+    O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, O.loss_cfg())
+    t3 = time.perf_counter()
+    return adv_s + rs_s + (t3 - t2), {"advantage_s": adv_s, "reshard_s": rs_s, "loss_port_s": t3 - t2}
+
+
+def cpu_baseline(records):
+    O, sb = cpu_sample()
+    nthreads = 8  # one thread per logical worker, as runner.hpp:525-530
+    cpu_step(O, sb, nthreads)  # warm-up
+    ts = [cpu_step(O, sb, nthreads)[0] for _ in range(2)]
+    t = min(ts)
+    return {"value": round(sb.n_tokens / t, 1), "unit": UNIT, "cores": nthreads, "kind": "reference",
+            "sample": f"{CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096] ({sb.n_tokens} tokens, 1/16 of C2): "
+                      "reference fn_group_advantage + BufferStore dp8->dp4 (B=1,W=8; 8 worker threads) "
+                      "+ oracle loss port (1 thread; the reference has no loss)",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    O, sb = cpu_sample()
+    nthreads = 8
+    for _ in range(max(args.warmup, 1)):
+        cpu_step(O, sb, nthreads)
+    steps = max(1, min(args.steps, 10))
+    ts, parts = [], None
+    for _ in range(steps):
+        t, parts = cpu_step(O, sb, nthreads)
+        ts.append(t)
+    t = sum(ts) / len(ts)
+    v = round(sb.n_tokens / t, 1)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": max(args.warmup, 1),
+            "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (keyed SplitMix64)", "impl": "reference",
+            "config": {"workload": f"bounded sample of C2: {CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096]",
+                       "tokens": sb.n_tokens, "phases_s": parts},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "reference",
+                             "sample": f"{sb.n_tokens} tokens; reference fn_group_advantage + BufferStore reshard "
+                                       "(oracle/_ref, compiled from /root/reference) + oracle loss port"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dfx(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * dfx.h -- C ABI of the B200-native DistFlow post-rollout hot path (libdfx.so).
+ *
+ * Plain C types, device pointers and sizes only; no torch types. Every entry
+ * point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/). The C++ drop-in shims
+ * that keep the reference's StageFn / FunctionRegistry / BufferStore API are
+ * in include/dfx_distflow.hpp; the Python mirror is paper_2507_13833_b200/.
+ *
+ * Conventions
+ *   - Return value: dfx_status (0 = OK). On failure dfx_last_error() returns a
+ *     thread-local message. Codes mirror the reference's typed exceptions
+ *     (distflow/errors.hpp), so shims can rethrow the same types.
+ *   - All compute calls are asynchronous on the given CUDA stream and never
+ *     allocate: scratch comes from a caller-provided workspace sized by the
+ *     matching *_workspace_bytes() query. Calls are re-entrant across threads
+ *     and devices (no global mutable state besides the error message).
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     returns DFX_CUDA_ERROR.
+ */
+#ifndef DFX_H
+#define DFX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dfx_stream; /* == cudaStream_t */
+typedef int32_t dfx_status;
+
+enum {
+  DFX_OK = 0,
+  DFX_ERROR = 1,                 /* distflow::Error                errors.hpp:10 */
+  DFX_LAYOUT_ERROR = 2,          /* LayoutError                    errors.hpp:32 */
+  DFX_INDIVISIBLE_ERROR = 3,     /* IndivisibleError               errors.hpp:52 */
+  DFX_MISSING_ROLLOUTS = 4,      /* MissingRolloutsError           errors.hpp:123 */
+  DFX_MISSING_CHANNEL = 5,       /* MissingChannelError            errors.hpp:116 */
+  DFX_STALE_ITERATION = 6,       /* StaleIterationError            errors.hpp:99 */
+  DFX_NOT_READY = 7,             /* NotReadyError                  errors.hpp:104 */
+  DFX_UNKNOWN_STAGE = 8,         /* UnknownStageError              errors.hpp:109 */
+  DFX_INVALID_ARGUMENT = 9,
+  DFX_CUDA_ERROR = 10,
+  DFX_NCCL_ERROR = 11,
+};
+
+const char* dfx_last_error(void);
+const char* dfx_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Packed batch (device SoA). Replaces the AoS SampleBatch / SampleRecord /
+ * Rollout model (distflow/record.hpp:17-41) on the device.
+ *
+ * A batch is n_records prompt records; record r owns rollouts
+ * [group_off[r], group_off[r+1]) (records are atomic, record.hpp:25-26);
+ * rollout s owns tokens [cu_seqlens[s], cu_seqlens[s+1]).
+ * cu_seqlens values are ABSOLUTE indices into the token streams, so a view of
+ * a sub-range of rollouts is just a pointer offset into group_off/cu_seqlens
+ * with the same token stream base pointers (zero-copy slicing).
+ * Token streams must be 16-byte aligned at index 0 and readable on
+ * [cu_seqlens[0] & ~7, (cu_seqlens[n_rollouts] + 7) & ~7) (kernels issue
+ * aligned 128-bit loads and discard the out-of-range lanes).
+ * Calls take token_base = cu_seqlens[0] and token_span =
+ * cu_seqlens[n_rollouts] - cu_seqlens[0] from the host (the packer knows them),
+ * so no call ever reads device memory on the host.
+ * Rollout channels are f64 (the reference's channel type, record.hpp:20).
+ * Pointers not needed by a call may be NULL.
+ * ------------------------------------------------------------------------- */
+typedef struct dfx_packed {
+  int64_t n_records;
+  int64_t n_rollouts;
+  const int32_t* group_off;   /* [n_records+1] rollout offsets, group_off[0]==0 */
+  const int32_t* roll_group;  /* [n_rollouts] record index of each rollout */
+  const int64_t* cu_seqlens;  /* [n_rollouts+1] absolute token offsets */
+  const double* reward;       /* [n_rollouts] channel "reward" */
+  const double* value;        /* [n_rollouts] channel "value" */
+  const float* lp;            /* current-policy log-probs */
+  const float* old_lp;        /* rollout-policy log-probs */
+  const float* ref_lp;        /* reference-policy log-probs */
+  const float* value_tok;     /* per-token critic values (GAE) */
+  const float* token_reward;  /* per-token rewards (GAE) */
+  const uint8_t* mask;        /* response mask, 0/1 */
+} dfx_packed;
+
+/* ---------------------------------------------------------------------------
+ * Advantages
+ * ------------------------------------------------------------------------- */
+
+/* Replaces fn_group_advantage (distflow/functions.hpp:143-161).
+ * Per record: f64 mean and population std of the rollouts' rewards,
+ * adv = d == 0 ? 0 : d / (std + eps). Bit-identical to the reference (same
+ * operation order, no FMA contraction). Writes adv_roll[n_rollouts] (f64).
+ * An empty record sets kFlagMissingRollouts in *flags (device, nullable);
+ * dfx_check_flags() turns it into DFX_MISSING_ROLLOUTS. */
+dfx_status dfx_grpo_advantage(const dfx_packed* b, double eps, double* adv_roll, int32_t* flags,
+                              dfx_stream stream);
+
+/* Per-token broadcast (new): adv_tok[t] = mask[t] ? f32(adv_roll[s]) : 0 for
+ * every token t of rollout s, indexed like the token streams. */
+dfx_status dfx_broadcast_advantage(const dfx_packed* b, int64_t token_base, int64_t token_span,
+                                   const double* adv_roll, float* adv_tok, dfx_stream stream);
+
+/* Replaces fn_ppo_advantage (distflow/functions.hpp:163-172): adv = reward - value. */
+dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream stream);
+
+/* GAE reverse scan (new; the reference has none). Per rollout:
+ *   m1 = t+1<L ? mask[t+1] : 0, v1 = t+1<L ? V[t+1] : 0
+ *   delta_t = r_t + gamma*m1*v1 - V_t ;  A_t = delta_t + gamma*lam*m1*A_{t+1} ;  R_t = A_t + V_t
+ * computed in f64 inside the kernel, stored f32. Optionally writes the masked
+ * whitening sums whiten[3] = {sum m*A, sum m*A^2, sum m} (device f64). */
+/* workspace (only when whiten != NULL) must be zero-filled once at allocation;
+ * the kernel leaves it zeroed again. */
+size_t dfx_gae_workspace_bytes(int64_t n_rollouts);
+dfx_status dfx_gae(const dfx_packed* b, double gamma, double lam, float* adv, float* ret,
+                   double* whiten, void* workspace, size_t ws_bytes, dfx_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * PPO / GRPO clipped surrogate + KL + masked aggregation (new; fills the
+ * fn_train slot, distflow/functions.hpp:176-182, node actor_train dag.hpp:335)
+ * ------------------------------------------------------------------------- */
+enum { DFX_KL_NONE = 0, DFX_KL_K1 = 1, DFX_KL_K2 = 2, DFX_KL_K3 = 3 };
+enum { DFX_AGG_TOKEN_MEAN = 0, DFX_AGG_SEQ_MEAN_TOKEN_MEAN = 1, DFX_AGG_SEQ_MEAN_TOKEN_SUM = 2 };
+enum {
+  DFX_ADV_GROUP_FUSED = 0, /* GRPO: group stats from b->reward computed in-kernel (bit-exact) */
+  DFX_ADV_ROLLOUT = 1,     /* per-rollout f64 advantage (adv_roll), broadcast to tokens */
+  DFX_ADV_TOKEN = 2,       /* per-token f32 advantage (adv_tok_in), e.g. from dfx_gae */
+};
+
+typedef struct dfx_loss_cfg {
+  double clip_low;   /* ratio clipped to [1-clip_low, 1+clip_high] */
+  double clip_high;
+  double beta;       /* KL coefficient */
+  double adv_eps;    /* DFX_ADV_GROUP_FUSED: StageContext::advantage_eps (functions.hpp:59) */
+  int32_t kl_type;   /* DFX_KL_* ; k3 is clamped to [-10, 10] */
+  int32_t agg;       /* DFX_AGG_* */
+  int32_t adv_source;/* DFX_ADV_* */
+  int32_t whiten;    /* 1: A_w = (A - mu) * rsqrt(var_unbiased + 1e-8), from whiten_sums */
+} dfx_loss_cfg;
+
+/* One per loss group (device memory), all f64. */
+typedef struct dfx_loss_out {
+  double loss, pg_loss, kl, clipfrac, approx_kl, n_tokens, n_seqs;
+} dfx_loss_out;
+
+typedef struct dfx_loss_args {
+  double* adv_roll;              /* DFX_ADV_ROLLOUT input; DFX_ADV_GROUP_FUSED output (nullable) */
+  const float* adv_tok_in;       /* DFX_ADV_TOKEN input */
+  const double* whiten_sums;     /* cfg.whiten: {sum m*A, sum m*A^2, sum m} (device) */
+  float* adv_tok_out;            /* nullable: per-token advantage actually used (after whitening) */
+  float* dlogp;                  /* nullable: d loss / d lp per token (extra mask pre-pass) */
+  int32_t n_loss_groups;         /* >=1; 0 treated as 1 */
+  const int32_t* loss_group_off; /* device [n_loss_groups+1] rollout offsets, NULL for one group */
+  dfx_loss_out* out;             /* device [n_loss_groups] */
+  int32_t* flags;                /* nullable device error flags (fused GRPO: empty record) */
+  void* ev_main_begin;           /* nullable cudaEvent_t recorded right before / after the streaming */
+  void* ev_main_end;             /*   kernel (roofline timing of the dominant kernel on its stream) */
+} dfx_loss_args;
+
+/* Workspace must be zero-filled once at allocation; every call leaves its
+ * ticket counters zeroed again. One launch of the fused streaming kernel plus
+ * one finalize launch (two more when dlogp is requested). */
+size_t dfx_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span, int32_t n_loss_groups);
+dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span,
+                        const dfx_loss_cfg* cfg,
+                        const dfx_loss_args* args, void* workspace, size_t ws_bytes,
+                        dfx_stream stream);
+
+/* Device-side error flags written by kernels (e.g. an empty record seen by the
+ * fused GRPO path). Reads flags (device int32) and returns the status. Syncs. */
+dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Synthetic rollouts on device: the same counter-keyed
+ * SplitMix64 values as the CPU generator (oracle/dfx_oracle.h), bit-exact.
+ * ids: device [n_records] sample ids; n_roll rollouts per record;
+ * cu_seqlens: device [n_records*n_roll+1]. Any output may be NULL.
+ * ------------------------------------------------------------------------- */
+dfx_status dfx_synth_tokens(uint64_t seed, const uint64_t* ids, int64_t n_records, int32_t n_roll,
+                            const int64_t* cu_seqlens, int64_t token_base, int64_t token_span, float* lp,
+                            float* old_lp, float* ref_lp, float* value_tok, float* token_reward,
+                            uint8_t* mask, int32_t* token_id, dfx_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Timing helpers (cudaEvent_t as void*), so ctypes callers can bracket a
+ * kernel on the stream it runs on.
+ * ------------------------------------------------------------------------- */
+dfx_status dfx_event_create(void** ev);
+dfx_status dfx_event_destroy(void* ev);
+dfx_status dfx_event_record(void* ev, dfx_stream stream);
+dfx_status dfx_event_elapsed_ms(void* ev_begin, void* ev_end, float* ms); /* syncs ev_end */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

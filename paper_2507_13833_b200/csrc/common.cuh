@@ -1,0 +1,143 @@
+// common.cuh -- shared device helpers for libdfx (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/dfx.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libdfx is written for sm_100a (B200) only"
+#endif
+
+namespace dfx {
+
+// ---- error plumbing (thread-local message, see dfx_last_error) -------------
+void set_error(const std::string& msg);
+dfx_status fail(dfx_status code, const std::string& msg);
+dfx_status cuda_status(cudaError_t e, const char* what);
+
+#define DFX_CUDA(call)                                            \
+  do {                                                            \
+    cudaError_t _e = (call);                                      \
+    if (_e != cudaSuccess) return ::dfx::cuda_status(_e, #call);  \
+  } while (0)
+
+#define DFX_LAUNCH_CHECK(what)                                        \
+  do {                                                                \
+    cudaError_t _e = cudaGetLastError();                              \
+    if (_e != cudaSuccess) return ::dfx::cuda_status(_e, what);       \
+  } while (0)
+
+constexpr int kWarp = 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// device error flags (bit per condition), reported by dfx_check_flags
+enum : int32_t { kFlagMissingRollouts = 1, kFlagBadInput = 2 };
+
+// ---- 128-bit streaming loads (read once: bypass L1 allocation) --------------
+__device__ __forceinline__ float4 ldg_stream_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_stream_f4(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ float f4_get(const float4& v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---- reference hash (distflow/hash.hpp), integer-exact on device ------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t hash_combine(uint64_t seed, uint64_t v) {
+  return splitmix64(seed ^ (v + 0x9E3779B97F4A7C15ull + (seed << 6) + (seed >> 2)));
+}
+__device__ __forceinline__ double unit_from_hash(uint64_t h) {
+  return __dmul_rn((double)(h >> 11), 1.0 / 9007199254740992.0);
+}
+__device__ __forceinline__ double symmetric_from_hash(uint64_t h) {
+  return __dadd_rn(__dmul_rn(2.0, unit_from_hash(h)), -1.0);
+}
+
+// ---- slot decomposition of a packed token range ------------------------------
+// Work units are the non-empty pieces "rollout s  ∩  window w" of the token
+// line, windows being 2^sh-token aligned blocks starting at base = cu[0] & ~3.
+// Piece (s, w) gets slot id s + w; slot ids are unique and increase along the
+// token line, so each rollout's pieces occupy contiguous slots
+// [s + w_first(s), s + w_last(s)] and a warp recovers (s, w) from its slot id
+// with a search over f(s) = s + ((cu[s] - base) >> sh), which is strictly
+// increasing. Slots whose piece is empty (a rollout starting exactly on a
+// window edge skips one id; zero-length rollouts own no slot) are no-ops.
+struct SlotGeom {
+  const int64_t* cu;
+  int64_t n_seq;
+  int64_t base;
+  int sh;
+};
+
+__device__ __forceinline__ int64_t slot_f(const SlotGeom& g, int64_t s) {
+  return s + ((__ldg(g.cu + s) - g.base) >> g.sh);
+}
+
+// Warp-cooperative 32-ary search: largest s in [0, n_seq) with f(s) <= u.
+__device__ __forceinline__ int64_t slot_find_seq(const SlotGeom& g, int64_t u, int lane) {
+  int64_t lo = 0, hi = g.n_seq;
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) >> 5;
+    const int64_t s = lo + (int64_t)lane * step;
+    const bool pred = (s < hi) && (slot_f(g, s) <= u);
+    const uint32_t m = __ballot_sync(kFull, pred);
+    const int k = 31 - __clz(m);  // lane 0 is always true: f(lo) <= u
+    lo = lo + (int64_t)k * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// Resolve slot u to (s, [t0, t1)); returns false for an empty slot.
+__device__ __forceinline__ bool slot_unit(const SlotGeom& g, int64_t u, int lane, int64_t& s,
+                                          int64_t& t0, int64_t& t1) {
+  s = slot_find_seq(g, u, lane);
+  const int64_t a = __ldg(g.cu + s), b = __ldg(g.cu + s + 1);
+  if (b <= a) return false;
+  const int64_t w = u - s;
+  const int64_t wa = (a - g.base) >> g.sh, wb = (b - 1 - g.base) >> g.sh;
+  if (w < wa || w > wb) return false;
+  const int64_t ws = g.base + (w << g.sh);
+  t0 = max(a, ws);
+  t1 = min(b, ws + ((int64_t)1 << g.sh));
+  return true;
+}
+
+// Host: number of slots for n_seq rollouts spanning token_span tokens.
+inline int64_t slot_count(int64_t n_seq, int64_t token_span, int sh) {
+  const int64_t win = ((token_span + 3) >> sh) + 2;  // base may start up to 3 before cu[0]
+  return n_seq + win;
+}
+
+}  // namespace dfx

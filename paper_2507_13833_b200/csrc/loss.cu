@@ -1,0 +1,763 @@
+// loss.cu -- GRPO group advantage (bit-exact vs fn_group_advantage), per-token
+// broadcast, and the fused advantage + PPO clipped surrogate + KL + masked
+// aggregation kernel over packed variable-length rollouts.
+//
+// Reference: distflow/functions.hpp:143-161 (fn_group_advantage),
+// :163-172 (fn_ppo_advantage), :176-182 (fn_train slot the loss fills).
+// HBM-bound streaming kernels: no tensor cores (no dense contraction).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dfx {
+
+// ---------------------------------------------------------------------------
+// GRPO group statistics, same operation order as functions.hpp:147-158 with
+// explicit round-to-nearest intrinsics so nvcc cannot contract into FMAs:
+// the f64 result is bit-identical to the reference's.
+// ---------------------------------------------------------------------------
+struct GroupStats {
+  double mean, denom;  // denom = std + eps
+};
+
+__device__ __forceinline__ GroupStats group_stats(const double* __restrict__ reward, int32_t r0,
+                                                  int32_t r1, double eps) {
+  const double n = (double)(r1 - r0);
+  double sum = 0.0;
+  for (int32_t i = r0; i < r1; ++i) sum = __dadd_rn(sum, __ldg(reward + i));
+  const double mean = __ddiv_rn(sum, n);
+  double var = 0.0;
+  for (int32_t i = r0; i < r1; ++i) {
+    const double d = __dsub_rn(__ldg(reward + i), mean);
+    var = __dadd_rn(var, __dmul_rn(d, d));
+  }
+  const double sd = __dsqrt_rn(__ddiv_rn(var, n));
+  return {mean, __dadd_rn(sd, eps)};
+}
+
+__device__ __forceinline__ double group_adv(double r, const GroupStats& g) {
+  const double d = __dsub_rn(r, g.mean);
+  return d == 0.0 ? 0.0 : __ddiv_rn(d, g.denom);
+}
+
+
+__global__ void ppo_adv_kernel(int64_t n, const double* __restrict__ reward,
+                               const double* __restrict__ value, double* __restrict__ adv) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) adv[s] = __dsub_rn(reward[s], value[s]);  // functions.hpp:169
+}
+
+// per-token broadcast adv_tok[t] = mask[t] ? f32(adv[s]) : 0, one warp per slot
+__global__ void __launch_bounds__(256) broadcast_kernel(SlotGeom g, int64_t n_slots,
+                                                        const double* __restrict__ adv,
+                                                        const uint8_t* __restrict__ mask,
+                                                        float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= n_slots) return;
+  int64_t s, t0, t1;
+  if (!slot_unit(g, u, lane, s, t0, t1)) return;
+  const float a = (float)__ldg(adv + s);
+  for (int64_t v = (t0 >> 2) + lane; v < ((t1 + 3) >> 2); v += 32) {
+    const uint32_t mk = ldg_stream_u32(mask + 4 * v);
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = ((mk >> (8 * k)) & 0xffu) ? a : 0.0f;
+    const int64_t t = 4 * v;
+    if (t >= t0 && t + 4 <= t1) {
+      stg_stream_f4(out + t, make_float4(o[0], o[1], o[2], o[3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (t + k >= t0 && t + k < t1) out[t + k] = o[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused loss
+// ---------------------------------------------------------------------------
+struct LossParams {
+  SlotGeom g;
+  int64_t n_slots;
+  int64_t n_records;
+  const int32_t* group_off;
+  const int32_t* roll_group;
+  const double* reward;
+  const float* lp;
+  const float* old_lp;
+  const float* ref_lp;
+  const uint8_t* mask;
+  const double* adv_roll_in;
+  const float* adv_tok_in;
+  double* adv_roll_out;
+  float* adv_tok_out;
+  float* dlogp;
+  const double* whiten_sums;
+  int whiten;
+  float clip_lo, clip_hi, beta;
+  double adv_eps;
+  int kl_type;
+  int agg;
+  int n_groups;
+  const int32_t* lgo;
+  const double* seq_n;     // dlogp: per-rollout mask count
+  const double* grp_stats; // dlogp: per loss group {N, S}
+  double* part;            // [5][n_slots]
+  int32_t* flags;
+  unsigned long long* ticket;  // [2] persistent-warp slot ticket, zero on entry, restored
+};
+
+__device__ __forceinline__ float k3_kl(float x) {
+  // e^x - x - 1 without cancellation for small |x| (x = ref - lp)
+  if (fabsf(x) < 0.5f) {
+    float p = 1.0f / 40320.0f;
+    p = fmaf(p, x, 1.0f / 5040.0f);
+    p = fmaf(p, x, 1.0f / 720.0f);
+    p = fmaf(p, x, 1.0f / 120.0f);
+    p = fmaf(p, x, 1.0f / 24.0f);
+    p = fmaf(p, x, 1.0f / 6.0f);
+    p = fmaf(p, x, 0.5f);
+    return x * x * p;
+  }
+  return expf(x) - x - 1.0f;
+}
+
+struct TokAcc {
+  float pg, kl, akl;
+  uint32_t clip, n;  // exact counts (a lane sees at most 2^sh tokens of a slot)
+};
+
+template <int ADV, bool DLOGP>
+__device__ __forceinline__ void loss_token(const LossParams& p, float A, float l, float o, float r,
+                                           float m, float w, TokAcc& acc, float& g) {
+  const float rho = __expf(l - o);
+  const float rc = fminf(fmaxf(rho, 1.0f - p.clip_lo), 1.0f + p.clip_hi);
+  const float pg1 = -A * rho, pg2 = -A * rc;
+  const bool clipped = pg2 > pg1;
+  const float pg = fmaxf(pg1, pg2);
+  float kl = 0.0f, dkl = 0.0f;
+  switch (p.kl_type) {
+    case DFX_KL_K1:
+      kl = l - r;
+      dkl = 1.0f;
+      break;
+    case DFX_KL_K2: {
+      const float d = l - r;
+      kl = 0.5f * d * d;
+      dkl = d;
+      break;
+    }
+    case DFX_KL_K3: {
+      const float x = r - l;
+      kl = k3_kl(x);
+      if (DLOGP) dkl = -expm1f(x);
+      if (kl > 10.0f) { kl = 10.0f; dkl = 0.0f; }
+      if (kl < -10.0f) { kl = -10.0f; dkl = 0.0f; }
+      break;
+    }
+    default:
+      break;
+  }
+  acc.pg += m * pg;
+  acc.kl += m * kl;
+  acc.clip += (clipped && m != 0.0f) ? 1u : 0u;
+  acc.akl += m * (o - l);
+  acc.n += m != 0.0f ? 1u : 0u;
+  if (DLOGP) g = m * w * ((clipped ? 0.0f : -A * rho) + p.beta * dkl);
+}
+
+// Group stats with all lanes participating: lanes load the rewards in
+// parallel, then every lane folds them in the reference's sequential order via
+// shuffles (identical result in every lane, no dependent global loads).
+__device__ __forceinline__ GroupStats group_stats_warp(const double* __restrict__ reward, int32_t r0, int32_t r1,
+                                                       double eps, int lane) {
+  const double n = (double)(r1 - r0);
+  double sum = 0.0;
+  for (int32_t base = r0; base < r1; base += 32) {
+    const int cnt = min(32, r1 - base);
+    const double x = lane < cnt ? __ldg(reward + base + lane) : 0.0;
+    for (int j = 0; j < cnt; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+  }
+  const double mean = __ddiv_rn(sum, n);
+  double var = 0.0;
+  for (int32_t base = r0; base < r1; base += 32) {
+    const int cnt = min(32, r1 - base);
+    const double x = lane < cnt ? __ldg(reward + base + lane) : 0.0;
+    const double d = __dsub_rn(x, mean);
+    const double dd = __dmul_rn(d, d);
+    for (int j = 0; j < cnt; ++j) var = __dadd_rn(var, __shfl_sync(kFull, dd, j));
+  }
+  const double sd = __dsqrt_rn(__ddiv_rn(var, n));
+  return {mean, __dadd_rn(sd, eps)};
+}
+
+// one warp per record
+__global__ void __launch_bounds__(256) grpo_adv_kernel(int64_t n_records, const int32_t* __restrict__ go,
+                                                       const double* __restrict__ reward, double eps,
+                                                       double* __restrict__ adv, int32_t* flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_records) return;
+  const int32_t a = go[r], b = go[r + 1];
+  if (b <= a) {  // require_rollouts functions.hpp:82-87
+    if (flags && lane == 0) atomicOr(flags, kFlagMissingRollouts);
+    return;
+  }
+  const GroupStats g = group_stats_warp(reward, a, b, eps, lane);
+  for (int32_t s = a + lane; s < b; s += 32) adv[s] = group_adv(__ldg(reward + s), g);
+}
+
+// Four tokens of one aligned vector. FULL: all four lie in [t0, t1).
+template <int ADV, bool DLOGP, bool FULL>
+__device__ __forceinline__ void loss_vec(const LossParams& p, float4 lv, float4 ov, float4 rv, float4 av, uint32_t mk,
+                                         int64_t t, int64_t t0, int64_t t1, float mu, float rstd, float w,
+                                         TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    bool on = ((mk >> (8 * k)) & 0xffu) != 0u;
+    if (!FULL) on = on && (t + k >= t0) && (t + k < t1);
+    const float m = on ? 1.0f : 0.0f;
+    float A = f4_get(av, k);
+    if (p.whiten) A = (A - mu) * rstd;
+    aout[k] = on ? A : 0.0f;
+    loss_token<ADV, DLOGP>(p, A, f4_get(lv, k), f4_get(ov, k), f4_get(rv, k), m, w, acc, gout[k]);
+  }
+}
+
+template <bool FULL>
+__device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, int64_t t1, const float (&v)[4]) {
+  if (FULL) {
+    stg_stream_f4(base + t, make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t + k >= t0 && t + k < t1) base[t + k] = v[k];
+  }
+}
+
+// Persistent warps; each warp repeatedly claims the next slot (atomic ticket)
+// and streams it: coalesced 128-bit loads of lp/old/ref (+adv) and 32-bit
+// mask words, kUnroll vectors per lane in flight, fused advantage broadcast,
+// clipped surrogate, KL and masked partial sums in registers (f32 per round,
+// f64 across rounds), one deterministic warp reduction per slot.
+template <int ADV, bool ADV_OUT, bool DLOGP>
+__global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+
+  // Record duty (fused GRPO mode): write the f64 advantage channel of every
+  // record, including zero-length rollouts that own no slot.
+  if (ADV == DFX_ADV_GROUP_FUSED && p.adv_roll_out) {
+    for (int64_t r = gwarp; r < p.n_records; r += nwarps) {
+      const int32_t a = __ldg(p.group_off + r), b = __ldg(p.group_off + r + 1);
+      if (b <= a) {
+        if (lane == 0 && p.flags) atomicOr(p.flags, kFlagMissingRollouts);
+        continue;
+      }
+      const GroupStats gs = group_stats_warp(p.reward, a, b, p.adv_eps, lane);
+      for (int32_t s = a + lane; s < b; s += 32) p.adv_roll_out[s] = group_adv(__ldg(p.reward + s), gs);
+    }
+  }
+
+  float mu = 0.0f, rstd = 1.0f;
+  if (p.whiten) {
+    const double N = p.whiten_sums[2];
+    const double m1 = N > 0 ? p.whiten_sums[0] / N : 0.0;
+    const double var = N > 1 ? (p.whiten_sums[1] - p.whiten_sums[0] * m1) / (N - 1.0) : 0.0;
+    mu = (float)m1;
+    rstd = (float)(1.0 / sqrt(fmax(var, 0.0) + 1e-8));
+  }
+  double* part = p.part;
+  unsigned long long* next = p.ticket;  // [0] next slot, [1] finished warps
+
+  for (;;) {
+    unsigned long long uu = 0;
+    if (lane == 0) uu = atomicAdd(next, 1ull);
+    const int64_t u = (int64_t)__shfl_sync(kFull, uu, 0);
+    if (u >= p.n_slots) break;
+
+    int64_t s, t0, t1;
+    if (!slot_unit(p.g, u, lane, s, t0, t1)) {
+      if (lane < 5) part[(int64_t)lane * p.n_slots + u] = 0.0;
+      continue;
+    }
+    float A_unit = 0.0f;
+    if (ADV == DFX_ADV_GROUP_FUSED) {
+      const int32_t grp = __ldg(p.roll_group + s);
+      const GroupStats gs = group_stats_warp(p.reward, __ldg(p.group_off + grp), __ldg(p.group_off + grp + 1),
+                                             p.adv_eps, lane);
+      A_unit = (float)group_adv(__ldg(p.reward + s), gs);
+    } else if (ADV == DFX_ADV_ROLLOUT) {
+      A_unit = (float)__ldg(p.adv_roll_in + s);
+    }
+    float w = 0.0f;
+    if (DLOGP) {
+      int gi = 0;
+      if (p.lgo)
+        while (gi + 1 < p.n_groups && __ldg(p.lgo + gi + 1) <= s) ++gi;
+      const double N = p.grp_stats[2 * gi], S = p.grp_stats[2 * gi + 1];
+      const double ns = p.seq_n[s];
+      if (p.agg == DFX_AGG_TOKEN_MEAN) w = N > 0 ? (float)(1.0 / N) : 0.0f;
+      else if (p.agg == DFX_AGG_SEQ_MEAN_TOKEN_MEAN) w = (S > 0 && ns > 0) ? (float)(1.0 / (S * ns)) : 0.0f;
+      else w = S > 0 ? (float)(1.0 / S) : 0.0f;
+    }
+
+    double dpg = 0.0, dkl = 0.0, dakl = 0.0;
+    uint32_t dclip = 0, dn = 0;
+    const int64_t vbeg = t0 >> 2;
+    const int32_t nvec = (int32_t)(((t1 + 3) >> 2) - vbeg);
+    const float* lp0 = p.lp + 4 * vbeg;
+    const float* ol0 = p.old_lp + 4 * vbeg;
+    const float* rf0 = p.ref_lp + 4 * vbeg;
+    const uint8_t* mk0 = p.mask + 4 * vbeg;
+    const float* ad0 = ADV == DFX_ADV_TOKEN ? p.adv_tok_in + 4 * vbeg : nullptr;
+    constexpr int kUnroll = 2;
+    for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
+      float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
+      uint32_t mk[kUnroll];
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        const int32_t i = ib + 32 * j;
+        if (i < nvec) {
+          lv[j] = ldg_stream_f4(lp0 + 4 * i);
+          ov[j] = ldg_stream_f4(ol0 + 4 * i);
+          rv[j] = ldg_stream_f4(rf0 + 4 * i);
+          mk[j] = ldg_stream_u32(mk0 + 4 * i);
+          if (ADV == DFX_ADV_TOKEN) av[j] = ldg_stream_f4(ad0 + 4 * i);
+        }
+      }
+      TokAcc acc{0.f, 0.f, 0.f, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        const int32_t i = ib + 32 * j;
+        if (i >= nvec) break;
+        const int64_t t = 4 * (vbeg + i);
+        if (ADV != DFX_ADV_TOKEN) av[j] = make_float4(A_unit, A_unit, A_unit, A_unit);
+        float aout[4], gout[4];
+        if (t >= t0 && t + 4 <= t1) {
+          loss_vec<ADV, DLOGP, true>(p, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout, gout);
+          if (ADV_OUT) store_vec<true>(p.adv_tok_out, t, t0, t1, aout);
+          if (DLOGP) store_vec<true>(p.dlogp, t, t0, t1, gout);
+        } else {
+          loss_vec<ADV, DLOGP, false>(p, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout, gout);
+          if (ADV_OUT) store_vec<false>(p.adv_tok_out, t, t0, t1, aout);
+          if (DLOGP) store_vec<false>(p.dlogp, t, t0, t1, gout);
+        }
+      }
+      dpg += acc.pg;
+      dkl += acc.kl;
+      dakl += acc.akl;
+      dclip += acc.clip;
+      dn += acc.n;
+    }
+    dpg = warp_sum(dpg);
+    dkl = warp_sum(dkl);
+    dclip = warp_sum(dclip);
+    dakl = warp_sum(dakl);
+    dn = warp_sum(dn);
+    if (lane == 0) {
+      part[u] = dpg;
+      part[p.n_slots + u] = dkl;
+      part[2 * p.n_slots + u] = (double)dclip;
+      part[3 * p.n_slots + u] = dakl;
+      part[4 * p.n_slots + u] = (double)dn;
+    }
+  }
+  // the last warp out restores the tickets for the next launch
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(next + 1, 1ull);
+    if (done == (unsigned long long)nwarps - 1) {
+      next[0] = 0ull;
+      next[1] = 0ull;
+    }
+  }
+}
+
+// mask-count pre-pass (dlogp weights): part[4][u] = sum of mask over the slot
+__global__ void __launch_bounds__(256) mask_count_kernel(SlotGeom g, int64_t n_slots,
+                                                         const uint8_t* __restrict__ mask,
+                                                         double* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= n_slots) return;
+  int64_t s, t0, t1;
+  if (!slot_unit(g, u, lane, s, t0, t1)) {
+    if (lane == 0) cnt[u] = 0.0;
+    return;
+  }
+  uint32_t c = 0;
+  for (int64_t v = (t0 >> 2) + lane; v < ((t1 + 3) >> 2); v += 32) {
+    const uint32_t mk = ldg_stream_u32(mask + 4 * v);
+    const int64_t t = 4 * v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t + k >= t0 && t + k < t1 && ((mk >> (8 * k)) & 0xffu)) ++c;
+  }
+  c = warp_sum(c);
+  if (lane == 0) cnt[u] = (double)c;
+}
+
+// ---------------------------------------------------------------------------
+// Finalize: per-rollout sums over its contiguous slots, then per loss group a
+// deterministic block reduction; the last block of each group (ticket order)
+// reduces the block partials in index order. COUNTS: the dlogp pre-pass.
+// ---------------------------------------------------------------------------
+constexpr int kFinThreads = 256;
+constexpr int kFinSeqPerThread = 1;
+
+struct FinParams {
+  SlotGeom g;
+  int64_t n_slots;
+  int n_groups;
+  const int32_t* lgo;
+  int agg;
+  double beta;
+  const double* part;   // [5][n_slots] (COUNTS: [1][n_slots] counts)
+  double* blk;          // [n_groups][nb][6]
+  unsigned int* ticket; // [n_groups], zero on entry, restored to zero
+  int nb;
+  double* seq_n;        // COUNTS: out per-rollout mask counts
+  double* grp_stats;    // COUNTS: out per group {N, S}
+  dfx_loss_out* out;    // !COUNTS: out per group
+};
+
+template <int NQ>
+__device__ __forceinline__ void block_sum(double (&v)[NQ], double* sh) {
+  // fixed-shape tree: warp xor-shuffle, then warp 0 over the per-warp values
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) sh[wid * NQ + q] = v[q];
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double x = lane < nw ? sh[lane * NQ + q] : 0.0;
+      v[q] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+template <bool COUNTS>
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
+  __shared__ double sh[(kFinThreads / 32) * 6];
+  __shared__ bool is_last;
+  const int gi = blockIdx.y;
+  const int64_t sr0 = f.lgo ? f.lgo[gi] : 0;
+  const int64_t sr1 = f.lgo ? f.lgo[gi + 1] : f.g.n_seq;
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // pg, kl, clip, akl, n, S
+  const int64_t first = sr0 + (int64_t)blockIdx.x * kFinThreads * kFinSeqPerThread;
+#pragma unroll
+  for (int j = 0; j < kFinSeqPerThread; ++j) {
+    const int64_t s = first + (int64_t)j * kFinThreads + threadIdx.x;
+    if (s >= sr1) break;
+    const int64_t a = f.g.cu[s], b = f.g.cu[s + 1];
+    double q[5] = {0, 0, 0, 0, 0};
+    if (b > a) {
+      const int64_t u0 = s + ((a - f.g.base) >> f.g.sh), u1 = s + ((b - 1 - f.g.base) >> f.g.sh);
+      for (int64_t u = u0; u <= u1; ++u) {
+        if (COUNTS) {
+          q[4] += f.part[u];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) q[k] += f.part[(int64_t)k * f.n_slots + u];
+        }
+      }
+    }
+    const double ns = q[4];
+    if (COUNTS) f.seq_n[s] = ns;
+    acc[2] += q[2];
+    acc[3] += q[3];
+    acc[4] += ns;
+    if (ns > 0) acc[5] += 1.0;
+    if (f.agg == DFX_AGG_TOKEN_MEAN) {
+      acc[0] += q[0];
+      acc[1] += q[1];
+    } else if (ns > 0) {
+      const double div = f.agg == DFX_AGG_SEQ_MEAN_TOKEN_MEAN ? ns : 1.0;
+      acc[0] += q[0] / div;
+      acc[1] += q[1] / div;
+    }
+  }
+  block_sum<6>(acc, sh);
+  double* blk = f.blk + ((int64_t)gi * f.nb + blockIdx.x) * 6;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) blk[q] = acc[q];
+    __threadfence();
+    const unsigned t = atomicAdd(f.ticket + gi, 1u);
+    is_last = (t == (unsigned)f.nb - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  const volatile double* vb = f.blk + (int64_t)gi * f.nb * 6;
+  for (int i = threadIdx.x; i < f.nb; i += kFinThreads)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tot[q] += vb[(int64_t)i * 6 + q];
+  block_sum<6>(tot, sh);
+  if (threadIdx.x == 0) {
+    const double N = tot[4], S = tot[5];
+    if (COUNTS) {
+      f.grp_stats[2 * gi] = N;
+      f.grp_stats[2 * gi + 1] = S;
+    } else {
+      const double denom = f.agg == DFX_AGG_TOKEN_MEAN ? N : S;
+      dfx_loss_out o;
+      o.pg_loss = denom > 0 ? tot[0] / denom : 0.0;
+      o.kl = denom > 0 ? tot[1] / denom : 0.0;
+      o.loss = o.pg_loss + f.beta * o.kl;
+      o.clipfrac = N > 0 ? tot[2] / N : 0.0;
+      o.approx_kl = N > 0 ? tot[3] / N : 0.0;
+      o.n_tokens = N;
+      o.n_seqs = S;
+      f.out[gi] = o;
+    }
+    f.ticket[gi] = 0u;  // ready for the next call
+  }
+}
+
+}  // namespace dfx
+
+using namespace dfx;
+
+namespace {
+
+constexpr int kSlotShift = 11;  // 2048-token windows
+constexpr int kWarpsPerBlock = 8;
+
+struct LossWs {
+  unsigned long long* slot_ticket;
+  double* part;
+  double* blk;
+  double* seq_n;
+  double* grp_stats;
+  unsigned int* ticket;
+  int nb;
+  size_t bytes;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t span, int32_t n_groups) {
+  LossWs w{};
+  const int64_t n_slots = slot_count(n_seq, span, kSlotShift);
+  w.nb = (int)std::max<int64_t>(1, (n_seq + kFinThreads * kFinSeqPerThread - 1) / (kFinThreads * kFinSeqPerThread));
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    char* p = b ? b + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  // ticket first: callers zero the workspace once at allocation, and the
+  // kernels restore it to zero on exit
+  w.ticket = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * 2 * size_t(n_groups)));
+  w.slot_ticket = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2));
+  w.part = reinterpret_cast<double*>(take(sizeof(double) * 5 * size_t(n_slots)));
+  w.blk = reinterpret_cast<double*>(take(sizeof(double) * 6 * size_t(n_groups) * size_t(w.nb)));
+  w.seq_n = reinterpret_cast<double*>(take(sizeof(double) * size_t(n_seq + 1)));
+  w.grp_stats = reinterpret_cast<double*>(take(sizeof(double) * 2 * size_t(n_groups)));
+  w.bytes = off;
+  return w;
+}
+
+SlotGeom geom_of(const dfx_packed* b, int64_t base) {
+  SlotGeom g;
+  g.cu = b->cu_seqlens;
+  g.n_seq = b->n_rollouts;
+  g.base = base;
+  g.sh = kSlotShift;
+  return g;
+}
+
+// persistent grid: as many 256-thread CTAs as fit on all SMs at once
+template <int ADV, bool AO, bool DL>
+void launch_slots(const LossParams& p, cudaStream_t st) {
+  static thread_local int cached_dev = -1, cached_blocks = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loss_slots_kernel<ADV, AO, DL>, 256, 0);
+    cached_blocks = sms * std::max(per_sm, 1);
+    cached_dev = dev;
+  }
+  loss_slots_kernel<ADV, AO, DL><<<cached_blocks, 256, 0, st>>>(p);
+}
+
+template <int ADV>
+void launch_slots_adv(const LossParams& p, cudaStream_t st, bool ao, bool dl) {
+  if (ao) {
+    if (dl) launch_slots<ADV, true, true>(p, st);
+    else launch_slots<ADV, true, false>(p, st);
+  } else {
+    if (dl) launch_slots<ADV, false, true>(p, st);
+    else launch_slots<ADV, false, false>(p, st);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+dfx_status dfx_grpo_advantage(const dfx_packed* b, double eps, double* adv_roll, int32_t* flags,
+                              dfx_stream stream) {
+  if (!b || !b->group_off || !b->reward || !adv_roll) return fail(DFX_INVALID_ARGUMENT, "dfx_grpo_advantage: null argument");
+  if (b->n_records <= 0) return DFX_OK;
+  grpo_adv_kernel<<<(unsigned)((b->n_records + 7) / 8), 256, 0, stream>>>(b->n_records, b->group_off, b->reward, eps,
+                                                                           adv_roll, flags);
+  DFX_LAUNCH_CHECK("grpo_adv_kernel");
+  return DFX_OK;
+}
+
+dfx_status dfx_broadcast_advantage(const dfx_packed* b, int64_t token_base, int64_t token_span,
+                                   const double* adv_roll, float* adv_tok, dfx_stream stream) {
+  if (!b || !b->cu_seqlens || !b->mask || !adv_roll || !adv_tok) return fail(DFX_INVALID_ARGUMENT, "dfx_broadcast_advantage: null argument");
+  if (b->n_rollouts <= 0) return DFX_OK;
+  const SlotGeom g = geom_of(b, token_base & ~int64_t(3));
+  const int64_t n_slots = slot_count(b->n_rollouts, token_span, kSlotShift);
+  broadcast_kernel<<<(unsigned)((n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, stream>>>(
+      g, n_slots, adv_roll, b->mask, adv_tok);
+  DFX_LAUNCH_CHECK("broadcast_kernel");
+  return DFX_OK;
+}
+
+dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream stream) {
+  if (!b || !adv_roll) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_advantage: null argument");
+  if (!b->reward) return fail(DFX_MISSING_CHANNEL, "missing channel 'reward'");
+  if (!b->value) return fail(DFX_MISSING_CHANNEL, "missing channel 'value'");
+  if (b->n_rollouts <= 0) return DFX_OK;
+  ppo_adv_kernel<<<(unsigned)((b->n_rollouts + 255) / 256), 256, 0, stream>>>(b->n_rollouts, b->reward, b->value, adv_roll);
+  DFX_LAUNCH_CHECK("ppo_adv_kernel");
+  return DFX_OK;
+}
+
+size_t dfx_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span, int32_t n_loss_groups) {
+  if (n_loss_groups < 1) n_loss_groups = 1;
+  return loss_ws_layout(nullptr, n_rollouts, token_span, n_loss_groups).bytes;
+}
+
+dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span, const dfx_loss_cfg* cfg,
+                        const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
+  if (!b || !cfg || !args || !args->out) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
+  if (b->n_rollouts <= 0) {
+    DFX_CUDA(cudaMemsetAsync(args->out, 0, sizeof(dfx_loss_out) * (args->n_loss_groups < 1 ? 1 : args->n_loss_groups), stream));
+    return DFX_OK;
+  }
+  if (!b->cu_seqlens || !b->lp || !b->old_lp || !b->ref_lp || !b->mask)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: packed batch lacks cu_seqlens/lp/old_lp/ref_lp/mask");
+  const int32_t ng = args->n_loss_groups < 1 ? 1 : args->n_loss_groups;
+  if (ng > 1 && !args->loss_group_off) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: loss_group_off required for >1 group");
+  switch (cfg->adv_source) {
+    case DFX_ADV_GROUP_FUSED:
+      if (!b->reward) return fail(DFX_MISSING_CHANNEL, "missing channel 'reward'");
+      if (!b->group_off || !b->roll_group) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: fused GRPO needs group_off/roll_group");
+      break;
+    case DFX_ADV_ROLLOUT:
+      if (!args->adv_roll) return fail(DFX_MISSING_CHANNEL, "missing channel 'advantage'");
+      break;
+    case DFX_ADV_TOKEN:
+      if (!args->adv_tok_in) return fail(DFX_MISSING_CHANNEL, "missing per-token advantage");
+      break;
+    default:
+      return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad adv_source");
+  }
+  if (cfg->whiten && !args->whiten_sums) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: whiten needs whiten_sums");
+  if (cfg->kl_type < 0 || cfg->kl_type > 3 || cfg->agg < 0 || cfg->agg > 2) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad kl_type/agg");
+  const int64_t S = b->n_rollouts;
+  const LossWs w = loss_ws_layout(workspace, S, token_span, ng);
+  if (!workspace || ws_bytes < w.bytes) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: workspace too small");
+  const SlotGeom g = geom_of(b, token_base & ~int64_t(3));
+  const int64_t n_slots = slot_count(S, token_span, kSlotShift);
+  const bool want_dl = args->dlogp != nullptr;
+
+  FinParams f{};
+  f.g = g;
+  f.n_slots = n_slots;
+  f.n_groups = ng;
+  f.lgo = args->loss_group_off;
+  f.agg = cfg->agg;
+  f.beta = cfg->beta;
+  f.nb = w.nb;
+  f.blk = w.blk;
+  f.seq_n = w.seq_n;
+  f.grp_stats = w.grp_stats;
+  f.out = args->out;
+  const dim3 fgrid((unsigned)w.nb, (unsigned)ng);
+
+  if (want_dl) {
+    mask_count_kernel<<<(unsigned)((n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock), 256, 0, stream>>>(g, n_slots, b->mask, w.part);
+    DFX_LAUNCH_CHECK("mask_count_kernel");
+    f.part = w.part;
+    f.ticket = w.ticket + ng;
+    finalize_kernel<true><<<fgrid, kFinThreads, 0, stream>>>(f);
+    DFX_LAUNCH_CHECK("finalize_kernel<counts>");
+  }
+
+  LossParams p{};
+  p.g = g;
+  p.n_slots = n_slots;
+  p.n_records = b->n_records;
+  p.group_off = b->group_off;
+  p.roll_group = b->roll_group;
+  p.reward = b->reward;
+  p.lp = b->lp;
+  p.old_lp = b->old_lp;
+  p.ref_lp = b->ref_lp;
+  p.mask = b->mask;
+  p.adv_roll_in = args->adv_roll;
+  p.adv_tok_in = args->adv_tok_in;
+  p.adv_roll_out = cfg->adv_source == DFX_ADV_GROUP_FUSED ? const_cast<double*>(args->adv_roll) : nullptr;
+  p.adv_tok_out = args->adv_tok_out;
+  p.dlogp = args->dlogp;
+  p.whiten_sums = args->whiten_sums;
+  p.whiten = cfg->whiten;
+  p.clip_lo = (float)cfg->clip_low;
+  p.clip_hi = (float)cfg->clip_high;
+  p.beta = (float)cfg->beta;
+  p.adv_eps = cfg->adv_eps;
+  p.kl_type = cfg->kl_type;
+  p.agg = cfg->agg;
+  p.n_groups = ng;
+  p.lgo = args->loss_group_off;
+  p.seq_n = w.seq_n;
+  p.grp_stats = w.grp_stats;
+  p.part = w.part;
+  p.flags = args->flags;
+  p.ticket = w.slot_ticket;
+  const bool ao = args->adv_tok_out != nullptr;
+  if (args->ev_main_begin) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_begin), stream));
+  switch (cfg->adv_source) {
+    case DFX_ADV_GROUP_FUSED: launch_slots_adv<DFX_ADV_GROUP_FUSED>(p, stream, ao, want_dl); break;
+    case DFX_ADV_ROLLOUT: launch_slots_adv<DFX_ADV_ROLLOUT>(p, stream, ao, want_dl); break;
+    default: launch_slots_adv<DFX_ADV_TOKEN>(p, stream, ao, want_dl); break;
+  }
+  DFX_LAUNCH_CHECK("loss_slots_kernel");
+  if (args->ev_main_end) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_end), stream));
+  f.part = w.part;
+  f.ticket = w.ticket;
+  finalize_kernel<false><<<fgrid, kFinThreads, 0, stream>>>(f);
+  DFX_LAUNCH_CHECK("finalize_kernel");
+  return DFX_OK;
+}
+
+dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream) {
+  int32_t h = 0;
+  DFX_CUDA(cudaMemcpyAsync(&h, flags, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  DFX_CUDA(cudaStreamSynchronize(stream));
+  if (h & kFlagMissingRollouts) return fail(DFX_MISSING_ROLLOUTS, "a record has no rollouts; generation has not run");
+  if (h) return fail(DFX_ERROR, "device reported invalid input");
+  return DFX_OK;
+}
+
+}  // extern "C"

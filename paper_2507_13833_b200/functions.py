@@ -1,0 +1,318 @@
+"""GPU stage functions behind the reference's operator API (distflow/functions.hpp).
+
+Same shapes as the reference: a StageFn is ``fn(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None``
+that mutates ``batch`` in place (adds channels/streams, leaves the rest untouched), dispatched
+through a FunctionRegistry under the reference's registry keys (functions.hpp:184-219), so a DAG built by
+``preset_dag`` binds to these GPU nodes unchanged. Errors are the reference's types (errors.py).
+
+Every compute step calls libdfx.so (csrc/); nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _abi, errors
+from .packed import PackedBatch, _ptr
+
+# ---- DAG vocabulary (distflow/dag.hpp:17-71) -------------------------------------------
+ROLES = ("ACTOR", "CRITIC", "REWARD", "REFERENCE", "NONE")
+NODE_TYPES = ("MODEL_INFERENCE", "MODEL_TRAIN", "COMPUTE")
+
+
+@dataclass
+class NodeSpec:
+    """distflow::NodeSpec (dag.hpp:57-71)."""
+    node_id: str
+    role: str = "NONE"
+    node_type: str = "COMPUTE"
+    func_tag: str | None = None
+    deps: list = field(default_factory=list)
+
+    def dispatch_key(self) -> str:  # dag.hpp:65-68
+        return self.func_tag if self.func_tag else f"{self.role}/{self.node_type}"
+
+
+def preset_dag(algorithm: str) -> list[NodeSpec]:
+    """distflow::preset_dag (dag.hpp:310-357): node ids, roles, types, func tags and deps of the presets."""
+    n = NodeSpec
+    a = algorithm.lower()
+    if a == "ppo":
+        return [n("actor_generate", "ACTOR", "MODEL_INFERENCE", "actor_generate"),
+                n("ref_inference", "REFERENCE", "MODEL_INFERENCE", "ref_logprob", ["actor_generate"]),
+                n("critic_inference", "CRITIC", "MODEL_INFERENCE", "value_inference", ["actor_generate"]),
+                n("reward_compute", "REWARD", "COMPUTE", "reward_compute", ["actor_generate"]),
+                n("advantage_compute", "NONE", "COMPUTE", "ppo_advantage",
+                  ["ref_inference", "critic_inference", "reward_compute"]),
+                n("actor_train", "ACTOR", "MODEL_TRAIN", "train_actor", ["advantage_compute"]),
+                n("critic_train", "CRITIC", "MODEL_TRAIN", "train_critic", ["advantage_compute"])]
+    if a == "grpo":
+        return [n("actor_generate", "ACTOR", "MODEL_INFERENCE", "actor_generate"),
+                n("ref_inference", "REFERENCE", "MODEL_INFERENCE", "ref_logprob", ["actor_generate"]),
+                n("reward_compute", "REWARD", "COMPUTE", "reward_compute", ["actor_generate"]),
+                n("group_advantage_compute", "NONE", "COMPUTE", "group_advantage", ["ref_inference", "reward_compute"]),
+                n("actor_train", "ACTOR", "MODEL_TRAIN", "train_actor", ["group_advantage_compute"])]
+    raise errors.Error(f"unknown algorithm '{algorithm}'")
+
+
+# ---- context -------------------------------------------------------------------------------
+@dataclass
+class LossConfig:
+    clip_low: float = 0.2
+    clip_high: float = 0.2
+    beta: float = 0.001
+    kl: str = "k3"
+    agg: str = "token-mean"
+    whiten: bool = False
+    want_grad: bool = False
+
+
+class Workspace:
+    """Caching device scratch, zero-filled at allocation (libdfx kernels leave their tickets zeroed)."""
+
+    def __init__(self):
+        self._bufs: dict = {}
+
+    def const(self, key, make):
+        """Small device constants (e.g. loss-group offsets) built once and reused."""
+        t = self._bufs.get(key)
+        if t is None:
+            t = make()
+            self._bufs[key] = t
+        return t
+
+    def get(self, key: str, nbytes: int, device) -> torch.Tensor:
+        t = self._bufs.get(key)
+        if t is None or t.numel() < nbytes or t.device != torch.device(device):
+            t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = t
+        return t
+
+
+@dataclass
+class StageContext:
+    """distflow::StageContext (functions.hpp:55-61) + the GPU path's loss/GAE settings and stream."""
+    run_seed: int = 0
+    advantage_eps: float = 1e-6
+    model_versions: dict | None = None
+    loss: LossConfig = field(default_factory=LossConfig)
+    gae_gamma: float = 1.0
+    gae_lambda: float = 0.95
+    stream: torch.cuda.Stream | None = None
+    workspace: Workspace = field(default_factory=Workspace)
+
+    def cuda_stream(self, device) -> int:
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(device)
+        return s.cuda_stream
+
+
+StageFn = Callable[[NodeSpec, PackedBatch, StageContext], None]
+
+
+# ---- checks mirroring detail::require_rollouts / channel_of (functions.hpp:82-93) ---------------
+def _require_rollouts(batch: PackedBatch) -> None:
+    go = batch.host_group_off
+    if go is not None and batch.n_records and (np.diff(go) <= 0).any():
+        r = int(np.argmax(np.diff(go) <= 0))
+        sid = int(batch.ids[r].item()) & 0xFFFFFFFFFFFFFFFF
+        raise errors.MissingRolloutsError(f"record {sid} has no rollouts; generation has not run")
+
+
+def _channel(batch: PackedBatch, name: str) -> torch.Tensor:
+    t = batch.channels.get(name)
+    if t is None:
+        raise errors.MissingChannelError(name)
+    return t
+
+
+def _stream(batch: PackedBatch, name: str) -> torch.Tensor:
+    t = batch.streams.get(name)
+    if t is None:
+        raise errors.MissingChannelError(name)
+    return t
+
+
+# ---- stage functions ------------------------------------------------------------------------
+def fn_group_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
+    """GPU fn_group_advantage (functions.hpp:143-161): f64, bit-identical; writes channel 'advantage'."""
+    _require_rollouts(batch)
+    _channel(batch, "reward")
+    adv = torch.empty(batch.n_rollouts, dtype=torch.float64, device=batch.device)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_grpo_advantage(C.byref(st), float(ctx.advantage_eps), _ptr(adv), None,
+                                             ctx.cuda_stream(batch.device)))
+    batch.channels["advantage"] = adv
+
+
+def fn_ppo_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
+    """GPU fn_ppo_advantage (functions.hpp:163-172): advantage = reward - value."""
+    _require_rollouts(batch)
+    _channel(batch, "reward")
+    _channel(batch, "value")
+    adv = torch.empty(batch.n_rollouts, dtype=torch.float64, device=batch.device)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_ppo_advantage(C.byref(st), _ptr(adv), ctx.cuda_stream(batch.device)))
+    batch.channels["advantage"] = adv
+
+
+def broadcast_advantage(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
+    """Per-token advantage stream adv_tok[t] = mask[t] ? f32(advantage[s]) : 0."""
+    adv = _channel(batch, "advantage")
+    _stream(batch, "mask")
+    out = torch.zeros_like(batch.streams["mask"], dtype=torch.float32)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_broadcast_advantage(C.byref(st), batch.token_base, batch.token_span, _ptr(adv),
+                                                  _ptr(out), ctx.cuda_stream(batch.device)))
+    batch.streams["advantage"] = out
+    return out
+
+
+def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
+    """GAE reverse scan (new func tag 'gae_advantage'): token streams 'advantage', 'returns' + whitening sums."""
+    _require_rollouts(batch)
+    for n in ("token_reward", "value_tok", "mask"):
+        _stream(batch, n)
+    like = batch.streams["token_reward"]
+    adv = torch.zeros_like(like)
+    ret = torch.zeros_like(like)
+    wsum = torch.zeros(3, dtype=torch.float64, device=batch.device)
+    nbytes = _abi.lib().dfx_gae_workspace_bytes(batch.n_rollouts)
+    ws = ctx.workspace.get("gae", nbytes, batch.device)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_gae(C.byref(st), float(ctx.gae_gamma), float(ctx.gae_lambda), _ptr(adv), _ptr(ret),
+                                  _ptr(wsum), _ptr(ws), ws.numel(), ctx.cuda_stream(batch.device)))
+    batch.streams["advantage"] = adv
+    batch.streams["returns"] = ret
+    batch.channels["_whiten_sums"] = wsum
+
+
+def ppo_loss(batch: PackedBatch, ctx: StageContext, adv_source: str | None = None, loss_group_off=None,
+             adv_tok_out: bool = False, events=None) -> dict:
+    """Fused advantage + clipped surrogate + KL + masked aggregation. Returns device tensors.
+
+    adv_source: 'group' (GRPO stats fused in-kernel from 'reward'), 'rollout' (channel 'advantage'),
+    'token' (stream 'advantage', e.g. GAE). Default: token stream if present, else rollout channel, else group.
+    """
+    cfg = ctx.loss
+    if adv_source is None:
+        adv_source = ("token" if "advantage" in batch.streams else
+                      "rollout" if "advantage" in batch.channels else "group")
+    for n in ("lp", "old_lp", "ref_lp", "mask"):
+        _stream(batch, n)
+    if adv_source == "group":
+        _require_rollouts(batch)
+        _channel(batch, "reward")
+    ng = 1 if loss_group_off is None else len(loss_group_off) - 1
+    dev = batch.device
+    out = torch.empty(ng * 7, dtype=torch.float64, device=dev)
+    adv_roll = None
+    if adv_source == "rollout":
+        adv_roll = _channel(batch, "advantage")
+    elif adv_source == "group":
+        adv_roll = torch.empty(batch.n_rollouts, dtype=torch.float64, device=dev)
+    adv_tok_in = _stream(batch, "advantage") if adv_source == "token" else None
+    whiten = batch.channels.get("_whiten_sums") if cfg.whiten else None
+    if cfg.whiten and whiten is None:
+        raise errors.Error("whitening needs GAE whitening sums (run gae_advantage first)")
+    # every token in [token_base, token_base + token_span) is written by the kernel: no zero-fill needed
+    aout = torch.empty_like(batch.streams["lp"]) if adv_tok_out else None
+    dlogp = torch.empty_like(batch.streams["lp"]) if cfg.want_grad else None
+    lgo = None
+    if loss_group_off is not None:
+        key = ("lgo", tuple(int(x) for x in loss_group_off))
+        lgo = ctx.workspace.const(key, lambda: torch.as_tensor(np.asarray(loss_group_off, np.int32)).to(dev))
+    c = _abi.LossCfg(cfg.clip_low, cfg.clip_high, cfg.beta, float(ctx.advantage_eps), _abi.KL[cfg.kl],
+                     _abi.AGG[cfg.agg], _abi.ADV[adv_source], int(cfg.whiten))
+    ev = events or (None, None)
+    a = _abi.LossArgs(_ptr(adv_roll), _ptr(adv_tok_in), _ptr(whiten), _ptr(aout), _ptr(dlogp), ng, _ptr(lgo),
+                      _ptr(out), None, ev[0], ev[1])
+    nbytes = _abi.lib().dfx_ppo_loss_workspace_bytes(batch.n_rollouts, batch.token_span, ng)
+    ws = ctx.workspace.get("loss", nbytes, dev)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_ppo_loss(C.byref(st), batch.token_base, batch.token_span, C.byref(c), C.byref(a),
+                                       _ptr(ws), ws.numel(), ctx.cuda_stream(dev)))
+    res = {"out": out.view(ng, 7)}
+    if adv_source == "group":
+        batch.channels["advantage"] = adv_roll
+    if aout is not None:
+        res["adv_tok"] = aout
+    if dlogp is not None:
+        res["dlogp"] = dlogp
+    return res
+
+
+def loss_dict(out_row: torch.Tensor) -> dict:
+    vals = out_row.detach().cpu().tolist()
+    return dict(zip(_abi.LOSS_OUT_FIELDS, vals))
+
+
+def fn_train(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
+    """GPU train node (fills fn_train's slot, functions.hpp:176-182): computes the PPO/GRPO loss on the device,
+    stores it as batch.channels['_loss'] (f64[7]), and bumps the role's model version like the reference."""
+    if node.role not in ("ACTOR", "CRITIC"):
+        raise errors.Error(f"role {node.role} is frozen and cannot train")
+    if node.role == "ACTOR":
+        res = ppo_loss(batch, ctx)
+        batch.channels["_loss"] = res["out"].reshape(-1)
+        if "dlogp" in res:
+            batch.streams["dlogp"] = res["dlogp"]
+    if ctx.model_versions is not None:
+        ctx.model_versions[node.role] = ctx.model_versions.get(node.role, 0) + 1
+
+
+# ---- registry (functions.hpp:184-249) -------------------------------------------------------------
+class FunctionRegistry:
+    def __init__(self):
+        self._fns: dict[str, StageFn] = {}
+
+    def register_fn(self, key: str, fn: StageFn) -> None:
+        if key in self._fns:
+            raise errors.Error(f"duplicate registration for key '{key}'")  # functions.hpp:187-189
+        self._fns[key] = fn
+
+    def find(self, key: str) -> StageFn | None:
+        return self._fns.get(key)
+
+    def keys(self):
+        return sorted(self._fns)
+
+
+def builtin_gpu_registry() -> FunctionRegistry:
+    """The GPU path under the reference's builtin_registry keys (functions.hpp:201-219) + 'gae_advantage'."""
+    reg = FunctionRegistry()
+    reg.register_fn("group_advantage", fn_group_advantage)
+    reg.register_fn("ppo_advantage", fn_ppo_advantage)
+    reg.register_fn("gae_advantage", fn_gae_advantage)
+    reg.register_fn("train_actor", fn_train)
+    reg.register_fn("train_critic", fn_train)
+    reg.register_fn("ACTOR/MODEL_TRAIN", fn_train)
+    reg.register_fn("CRITIC/MODEL_TRAIN", fn_train)
+    return reg
+
+
+def registry_bind(chain: list[NodeSpec], registry: FunctionRegistry, layouts: dict):
+    """registry_bind (functions.hpp:234-249): UnboundNodeError / LayoutError like the reference."""
+    out = []
+    for spec in chain:
+        key = spec.dispatch_key()
+        fn = registry.find(key)
+        if fn is None:
+            raise errors.UnboundNodeError(spec.node_id, key)
+        if spec.node_id not in layouts:
+            raise errors.LayoutError(f"no layout for stage '{spec.node_id}'")
+        out.append((spec, key, fn, layouts[spec.node_id]))
+    return out
+
+
+def invoke_node(spec: NodeSpec, fn: StageFn, batch: PackedBatch, ctx: StageContext) -> None:
+    """detail::invoke_node (worker.hpp:192-200): FunctionError passes through, everything else is wrapped."""
+    try:
+        fn(spec, batch, ctx)
+    except errors.FunctionError:
+        raise
+    except Exception as e:  # noqa: BLE001
+        raise errors.FunctionError(spec.node_id, str(e)) from e

@@ -1,0 +1,48 @@
+"""Shared test helpers: build matching host (oracle) and device batches, and the tolerance definition.
+
+TOLERANCE (written once, used by every floating-point parity test):
+  advantages / GAE / per-token outputs:  |x - y| <= 1e-5 * max(|y|, rms(y))
+  loss scalars:                          |x - y| <= 1e-5 * max(|y|, s)  with s = mean |per-token term|
+The norm floor is needed because advantages, GAE outputs and mean-zero loss terms cross zero
+(SURVEY.md App. B.6); it is the "1e-5 relative" of north_star stated for values near zero.
+Integer, index, byte and f64 group-advantage results are compared bit-exactly.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+RTOL = 1e-5
+
+
+def assert_close_vec(x, y, what=""):
+    x = np.asarray(x, np.float64)
+    y = np.asarray(y, np.float64)
+    assert x.shape == y.shape, (what, x.shape, y.shape)
+    if y.size == 0:
+        return
+    rms = float(np.sqrt(np.mean(y * y)))
+    tol = RTOL * np.maximum(np.abs(y), rms)
+    bad = np.abs(x - y) > tol
+    assert not bad.any(), (f"{what}: {int(bad.sum())} of {y.size} outside tolerance; worst at "
+                           f"{int(np.argmax(np.abs(x - y) - tol))}: {x[np.argmax(np.abs(x - y) - tol)]} vs "
+                           f"{y[np.argmax(np.abs(x - y) - tol)]}")
+
+
+def assert_close_scalar(x, y, scale, what=""):
+    tol = RTOL * max(abs(y), scale)
+    assert abs(x - y) <= tol, f"{what}: {x} vs {y} (tol {tol})"
+
+
+def loss_term_scales(sb, adv_tok, cfg):
+    """mean |term| per loss scalar, computed in f64 from the same inputs (tolerance floor)."""
+    T = sb.n_tokens
+    m = sb.mask[:T].astype(np.float64)
+    lp, old, ref = (a[:T].astype(np.float64) for a in (sb.lp, sb.old_lp, sb.ref_lp))
+    A = np.abs(adv_tok[:T].astype(np.float64))
+    rho = np.exp(lp - old)
+    n = max(m.sum(), 1.0)
+    pg = (m * A * np.maximum(rho, 1.2)).sum() / n
+    x = ref - lp
+    kl = (m * (np.abs(np.expm1(x) - x) + np.abs(x) + 0.5 * x * x)).sum() / n
+    akl = (m * np.abs(old - lp)).sum() / n
+    return {"pg_loss": pg, "kl": kl, "loss": pg + cfg.beta * kl, "approx_kl": akl, "clipfrac": 1.0}

@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through libdfx's C ABI) against the CPU oracle on identical seeded inputs.
+
+Bit-exact: synthetic token streams, GRPO group advantage (f64) and its per-token broadcast.
+Within the tolerance in tests/helpers.py: GAE, PPO clipped surrogate + KL + aggregation, dlogp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import assert_close_scalar, assert_close_vec, loss_term_scales
+
+pytestmark = pytest.mark.gpu
+
+STREAMS = ("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward")
+
+
+def device_batch(dfx, sb, streams=STREAMS):
+    """Upload an oracle SynthBatch (host) to a device PackedBatch."""
+    st = {k: getattr(sb, k)[: sb.n_tokens] for k in streams if getattr(sb, k) is not None}
+    return dfx.PackedBatch.from_host(sb.ids, sb.group_off, sb.cu_seqlens, {"reward": sb.reward, "value": sb.value}, st)
+
+
+def make(O, seed, R, n, kind, lo, hi, streams=STREAMS):
+    return O.SynthBatch(seed, R, n, O.token_dist(kind, lo, lo, hi), streams=streams)
+
+
+CASES = [
+    # seed, records, rollouts, dist, min, max
+    (1, 64, 8, "constant", 1024, 1024),      # C1 shape
+    (7, 16, 2, "uniform", 16, 48),           # configs/grpo_small.json generation
+    (3, 37, 5, "uniform", 1, 300),           # ragged, many window crossings
+    (5, 8, 4, "uniform", 1, 3),              # tiny rollouts, many per window
+    (11, 20, 16, "skewed", 1, 16384),        # C5-like skewed lengths
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_device_synth_bit_exact(O, dfx, case):
+    seed, R, n, kind, lo, hi = case
+    sb = make(O, seed, R, n, kind, lo, hi, streams=STREAMS + ("token_id",))
+    dist = dfx.TokenDist(kind, lo, lo, hi)
+    db = dfx.PackedBatch.synthetic(seed, R, n, dist, streams=STREAMS + ("token_id",))
+    torch.cuda.synchronize()
+    assert db.host_cu.tolist() == sb.cu_seqlens.tolist()
+    T = sb.n_tokens
+    for k in STREAMS + ("token_id",):
+        got = db.streams[k][:T].cpu().numpy()
+        ref = getattr(sb, k)[:T]
+        assert got.tobytes() == ref.tobytes(), k
+    assert db.channels["reward"].cpu().numpy().tobytes() == sb.reward.tobytes()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_grpo_advantage_bit_exact(O, dfx, case):
+    seed, R, n, kind, lo, hi = case
+    sb = make(O, seed, R, n, kind, lo, hi)
+    db = device_batch(dfx, sb)
+    ctx = dfx.StageContext()
+    dfx.fn_group_advantage(dfx.NodeSpec("adv"), db, ctx)
+    got = db.channels["advantage"].cpu().numpy()
+    ref = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    assert got.tobytes() == ref.tobytes()
+    if O.ref_available():  # the reference itself, compiled from /root/reference
+        R_ = O.ref()
+        out = np.zeros_like(ref)
+        assert R_.ref_advantage(0, sb.n_records, O.ptr(sb.group_off), O.ptr(sb.reward), None, 1e-6, O.ptr(out)) == 0
+        assert got.tobytes() == out.tobytes()
+    from paper_2507_13833_b200.functions import broadcast_advantage
+    tok = broadcast_advantage(db, ctx)[: sb.n_tokens].cpu().numpy()
+    assert tok.tobytes() == O.broadcast_advantage(sb.cu_seqlens, ref, sb.mask)[: sb.n_tokens].tobytes()
+
+
+def test_grpo_advantage_kats(dfx):
+    """tests/test_functions.cpp:134-168 through the GPU path."""
+    def adv(rewards, eps):
+        S = len(rewards)
+        b = dfx.PackedBatch.from_host([0], [0, S], np.zeros(S + 1, np.int64), {"reward": np.array(rewards)})
+        ctx = dfx.StageContext(advantage_eps=eps)
+        dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
+        return b.channels["advantage"].cpu().numpy()
+    assert adv([1.0, 0.0, 1.0, 0.0], 0.0).tolist() == [1.0, -1.0, 1.0, -1.0]
+    z = adv([0.75, 0.75, 0.75], 0.0)
+    assert z.tolist() == [0.0, 0.0, 0.0] and np.isfinite(z).all()
+    assert adv([1.0, 0.0], 0.0)[0] > adv([1.0, 0.0], 0.5)[0]
+
+
+def test_ppo_advantage_and_errors(dfx):
+    """tests/test_functions.cpp:170-192 through the GPU path."""
+    b = dfx.PackedBatch.from_host([0], [0, 2], np.zeros(3, np.int64), {"reward": np.array([0.9, 0.2]),
+                                                                         "value": np.array([0.4, -0.1])})
+    dfx.fn_ppo_advantage(dfx.NodeSpec("a"), b, dfx.StageContext())
+    assert b.channels["advantage"].cpu().numpy().tolist() == [0.9 - 0.4, 0.2 - (-0.1)]
+    missing = dfx.PackedBatch.from_host([0], [0, 1], np.zeros(2, np.int64), {"reward": np.array([0.9])})
+    with pytest.raises(dfx.errors.MissingChannelError):
+        dfx.fn_ppo_advantage(dfx.NodeSpec("a"), missing, dfx.StageContext())
+    empty = dfx.PackedBatch.from_host([0, 1], [0, 1, 1], np.zeros(2, np.int64), {"reward": np.array([0.5])})
+    with pytest.raises(dfx.errors.MissingRolloutsError):
+        dfx.fn_group_advantage(dfx.NodeSpec("a"), empty, dfx.StageContext())
+
+
+LOSS_CFGS = [
+    dict(kl="k3", agg="token-mean"),
+    dict(kl="k1", agg="seq-mean-token-mean"),
+    dict(kl="k2", agg="seq-mean-token-sum"),
+    dict(kl="none", agg="token-mean", clip_low=0.1, clip_high=0.28),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("lc", LOSS_CFGS)
+@pytest.mark.parametrize("src", ["group", "rollout"])
+def test_fused_grpo_loss(O, dfx, case, lc, src):
+    seed, R, n, kind, lo, hi = case
+    sb = make(O, seed, R, n, kind, lo, hi)
+    db = device_batch(dfx, sb)
+    ctx = dfx.StageContext()
+    ctx.loss = dfx.LossConfig(want_grad=True, **lc)
+    adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    if src == "rollout":
+        dfx.fn_group_advantage(dfx.NodeSpec("a"), db, ctx)
+    res = dfx.ppo_loss(db, ctx, adv_source=src, adv_tok_out=True)
+    got = dfx.loss_dict(res["out"][0])
+    adv_tok = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
+    cfg = O.loss_cfg(kl=lc["kl"], agg=lc["agg"], clip_low=lc.get("clip_low", 0.2), clip_high=lc.get("clip_high", 0.2))
+    ref, g = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, cfg, want_grad=True)
+    T = sb.n_tokens
+    assert res["adv_tok"][:T].cpu().numpy().tobytes() == adv_tok[:T].tobytes()
+    if src == "group":
+        assert db.channels["advantage"].cpu().numpy().tobytes() == adv.tobytes()
+    sc = loss_term_scales(sb, adv_tok, cfg)
+    assert got["n_tokens"] == ref["n_tokens"] and got["n_seqs"] == ref["n_seqs"]
+    for k in ("loss", "pg_loss", "kl", "approx_kl", "clipfrac"):
+        assert_close_scalar(got[k], ref[k], sc[k] if lc["agg"] == "token-mean" else max(sc[k], abs(ref[k])), k)
+    assert_close_vec(res["dlogp"][:T].cpu().numpy(), g[:T], "dlogp")
+
+
+@pytest.mark.parametrize("whiten", [False, True])
+def test_gae_and_ppo_loss(O, dfx, whiten):
+    """C3-like (scaled down): GAE reverse scan + whitening + clipped surrogate with per-token advantages."""
+    sb = make(O, 2, 24, 1, "uniform", 1, 5000)
+    db = device_batch(dfx, sb)
+    ctx = dfx.StageContext(gae_gamma=1.0, gae_lambda=0.95)
+    ctx.loss = dfx.LossConfig(whiten=whiten)
+    dfx.fn_gae_advantage(dfx.NodeSpec("gae"), db, ctx)
+    A, Rt, ws = O.gae(sb.cu_seqlens, sb.token_reward, sb.value_tok, sb.mask, 1.0, 0.95)
+    T = sb.n_tokens
+    assert_close_vec(db.streams["advantage"][:T].cpu().numpy(), A[:T], "gae adv")
+    assert_close_vec(db.streams["returns"][:T].cpu().numpy(), Rt[:T], "gae ret")
+    wsg = db.channels["_whiten_sums"].cpu().numpy()
+    assert wsg[2] == ws[2]
+    assert_close_vec(wsg[:2], ws[:2], "whiten sums")
+    res = dfx.ppo_loss(db, ctx, adv_source="token")
+    got = dfx.loss_dict(res["out"][0])
+    adv_f32 = db.streams["advantage"].cpu().numpy()  # the loss consumes the stored f32 advantages
+    cfg = O.loss_cfg(whiten=whiten)
+    ref, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_f32, sb.mask, cfg)
+    sc = loss_term_scales(sb, adv_f32, cfg)
+    for k in ("loss", "pg_loss", "kl", "approx_kl", "clipfrac"):
+        assert_close_scalar(got[k], ref[k], sc[k] * (3.0 if whiten else 1.0), k)
+
+
+def test_gae_kat(dfx):
+    """Hand-computed: one rollout r=[0,0,1], V=[0.5,0.5,0.5], mask=1, gamma=1, lam=0.5."""
+    cu = np.array([0, 3], np.int64)
+    streams = {"token_reward": np.array([0, 0, 1], np.float32), "value_tok": np.full(3, 0.5, np.float32),
+               "mask": np.ones(3, np.uint8)}
+    b = dfx.PackedBatch.from_host([0], [0, 1], cu, {}, streams)
+    dfx.fn_gae_advantage(dfx.NodeSpec("g"), b, dfx.StageContext(gae_gamma=1.0, gae_lambda=0.5))
+    # delta = [0+.5-.5, 0+.5-.5, 1-.5] = [0, 0, .5]; A2=.5, A1=0+.5*.5=.25, A0=.125
+    assert b.streams["advantage"][:3].cpu().numpy().tolist() == [0.125, 0.25, 0.5]
+    assert b.streams["returns"][:3].cpu().numpy().tolist() == [0.625, 0.75, 1.0]
+
+
+def test_loss_groups_match_slices(O, dfx):
+    """Per-loss-group outputs equal the oracle run on each group's rollout slice."""
+    sb = make(O, 9, 32, 4, "uniform", 1, 700)
+    db = device_batch(dfx, sb)
+    ctx = dfx.StageContext()
+    lgo = [0, 40, 41, 100, 128]
+    res = dfx.ppo_loss(db, ctx, adv_source="group", loss_group_off=lgo)
+    out = res["out"].cpu().numpy()
+    adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    adv_tok = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
+    cfg = O.loss_cfg()
+    for g in range(len(lgo) - 1):
+        cu = np.ascontiguousarray(sb.cu_seqlens[lgo[g]:lgo[g + 1] + 1])
+        ref, _ = O.ppo_loss(cu, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, cfg)
+        assert out[g][5] == ref["n_tokens"]
+        assert_close_scalar(out[g][0], ref["loss"], 1.0, f"group {g} loss")
+
+
+def test_empty_and_degenerate(O, dfx):
+    ctx = dfx.StageContext()
+    # zero-length rollouts mixed in, and a fully masked rollout
+    cu = np.array([0, 0, 5, 5, 9], np.int64)
+    T = 9
+    rng = np.random.default_rng(0)
+    streams = {"lp": -rng.random(T).astype(np.float32), "old_lp": -rng.random(T).astype(np.float32),
+               "ref_lp": -rng.random(T).astype(np.float32), "mask": np.array([1, 1, 0, 1, 1, 0, 0, 0, 0], np.uint8)}
+    b = dfx.PackedBatch.from_host([3, 4], [0, 2, 4], cu, {"reward": np.array([0.1, 0.9, 0.5, 0.5])}, streams)
+    res = dfx.ppo_loss(b, ctx, adv_source="group")
+    got = dfx.loss_dict(res["out"][0])
+    adv = O.grpo_advantage(np.array([0, 2, 4], np.int32), np.array([0.1, 0.9, 0.5, 0.5]), 1e-6)
+    assert b.channels["advantage"].cpu().numpy().tobytes() == adv.tobytes()
+    adv_tok = O.broadcast_advantage(cu, adv, streams["mask"])
+    ref, _ = O.ppo_loss(cu, streams["lp"], streams["old_lp"], streams["ref_lp"], adv_tok, streams["mask"],
+                        O.loss_cfg())
+    assert got["n_tokens"] == ref["n_tokens"] == 4
+    assert got["n_seqs"] == ref["n_seqs"] == 1
+    assert_close_scalar(got["loss"], ref["loss"], 1.0, "loss")
+    # empty batch
+    e = dfx.PackedBatch.from_host(np.zeros(0, np.uint64), [0], np.zeros(1, np.int64), {"reward": np.zeros(0)},
+                                  {k: np.zeros(0, np.float32) for k in ("lp", "old_lp", "ref_lp")} |
+                                  {"mask": np.zeros(0, np.uint8)})
+    r = dfx.ppo_loss(e, ctx, adv_source="group")
+    assert dfx.loss_dict(r["out"][0])["n_tokens"] == 0.0
+
+
+def test_c2_scale_properties(dfx):
+    """Full C2 size (1024 x 16 x U[1,4096], ~33.6M tokens): properties that need no CPU oracle pass.
+
+    - the fused path's per-rollout advantage equals the standalone GRPO kernel's bit for bit
+    - per-group advantage sums are ~0 (population-normalised), token count equals the mask sum
+    - the run is deterministic: a second call gives bit-identical loss scalars
+    """
+    db = dfx.PackedBatch.synthetic(1, 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096))
+    ctx = dfx.StageContext()
+    r1 = dfx.ppo_loss(db, ctx, adv_source="group")["out"].clone()
+    fused_adv = db.channels["advantage"].clone()
+    r2 = dfx.ppo_loss(db, ctx, adv_source="group")["out"]
+    assert r1.cpu().numpy().tobytes() == r2.cpu().numpy().tobytes()
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), db, ctx)
+    assert db.channels["advantage"].cpu().numpy().tobytes() == fused_adv.cpu().numpy().tobytes()
+    a = fused_adv.cpu().numpy().reshape(1024, 16)
+    assert np.abs(a.sum(1)).max() < 1e-9
+    m = db.streams["mask"][: db.token_span].to(torch.float64).sum().item()
+    assert r1[0, 5].item() == m
