@@ -108,63 +108,102 @@ struct LossParams {
   unsigned long long* ticket;  // [2] persistent-warp slot ticket, zero on entry, restored
 };
 
-__device__ __forceinline__ float k3_kl(float x) {
-  // e^x - x - 1 without cancellation for small |x| (x = ref - lp)
-  if (fabsf(x) < 0.5f) {
-    float p = 1.0f / 40320.0f;
-    p = fmaf(p, x, 1.0f / 5040.0f);
-    p = fmaf(p, x, 1.0f / 720.0f);
-    p = fmaf(p, x, 1.0f / 120.0f);
-    p = fmaf(p, x, 1.0f / 24.0f);
-    p = fmaf(p, x, 1.0f / 6.0f);
-    p = fmaf(p, x, 0.5f);
-    return x * x * p;
-  }
-  return expf(x) - x - 1.0f;
+// ---- per-token math ---------------------------------------------------------
+// k3 = e^x - x - 1 (x = ref - lp) by its Taylor series for |x| < 1/8
+// (truncation < 1.2e-8 relative); callers fall back to expm1f(x) - x, which
+// has no cancellation, for the rare larger |x| (per vector, warp-uniform).
+__device__ __forceinline__ float k3_series(float x) {
+  float q = 1.0f / 720.0f;
+  q = fmaf(q, x, 1.0f / 120.0f);
+  q = fmaf(q, x, 1.0f / 24.0f);
+  q = fmaf(q, x, 1.0f / 6.0f);
+  q = fmaf(q, x, 0.5f);
+  return (x * x) * q;
 }
+constexpr float kK3Series = 0.125f;
+constexpr float kLog2e = 1.4426950408889634f;
 
 struct TokAcc {
-  float pg, kl, akl;
-  uint32_t clip, n;  // exact counts (a lane sees at most 2^sh tokens of a slot)
+  float pg, kl, akl, clip, n;
 };
 
-template <int ADV, bool DLOGP>
-__device__ __forceinline__ void loss_token(const LossParams& p, float A, float l, float o, float r,
-                                           float m, float w, TokAcc& acc, float& g) {
-  const float rho = __expf(l - o);
-  const float rc = fminf(fmaxf(rho, 1.0f - p.clip_lo), 1.0f + p.clip_hi);
-  const float pg1 = -A * rho, pg2 = -A * rc;
-  const bool clipped = pg2 > pg1;
-  const float pg = fmaxf(pg1, pg2);
-  float kl = 0.0f, dkl = 0.0f;
-  switch (p.kl_type) {
-    case DFX_KL_K1:
-      kl = l - r;
-      dkl = 1.0f;
-      break;
-    case DFX_KL_K2: {
-      const float d = l - r;
-      kl = 0.5f * d * d;
-      dkl = d;
-      break;
+// Per-unit constants for a warp-uniform advantage A (GRPO broadcast): with
+// s = sign(A), the clipped surrogate max(-A rho, -A clip(rho)) equals
+// -|A| * min(s rho, s bound) where bound = 1+eps_hi (A>0) or 1-eps_lo (A<0),
+// and the clip fires iff s rho > s bound. A == 0 gives bound = +inf: pg = 0,
+// never clipped -- identical to the reference formula.
+struct UnitAdv {
+  float A, nA, s, sb;
+};
+__device__ __forceinline__ UnitAdv unit_adv(float A, float lo, float hi) {
+  UnitAdv u;
+  u.A = A;
+  u.nA = -fabsf(A);
+  u.s = A < 0.0f ? -1.0f : 1.0f;
+  u.sb = A > 0.0f ? hi : (A < 0.0f ? -lo : __int_as_float(0x7f800000));
+  return u;
+}
+
+// Four tokens of one aligned vector starting at token t. FULL: all in range.
+template <int ADV, int KL, bool DLOGP, bool FULL>
+__device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua, float4 lv, float4 ov, float4 rv,
+                                         float4 av, uint32_t mk, int64_t t, int64_t t0, int64_t t1, float mu,
+                                         float rstd, float w, TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
+  const float lo = 1.0f - p.clip_lo, hi = 1.0f + p.clip_hi;
+  float x[4], kl[4], dkl[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[k] = f4_get(rv, k) - f4_get(lv, k);
+  if (KL == DFX_KL_K3) {
+    const float ax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+    if (ax < kK3Series) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) kl[k] = k3_series(x[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) kl[k] = fminf(fmaxf(expm1f(x[k]) - x[k], -10.0f), 10.0f);
     }
-    case DFX_KL_K3: {
-      const float x = r - l;
-      kl = k3_kl(x);
-      if (DLOGP) dkl = -expm1f(x);
-      if (kl > 10.0f) { kl = 10.0f; dkl = 0.0f; }
-      if (kl < -10.0f) { kl = -10.0f; dkl = 0.0f; }
-      break;
-    }
-    default:
-      break;
+    if (DLOGP)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dkl[k] = (kl[k] >= 10.0f || kl[k] <= -10.0f) ? 0.0f : -expm1f(x[k]);
+  } else if (KL == DFX_KL_K1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { kl[k] = -x[k]; dkl[k] = 1.0f; }
+  } else if (KL == DFX_KL_K2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { kl[k] = 0.5f * x[k] * x[k]; dkl[k] = -x[k]; }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { kl[k] = 0.0f; dkl[k] = 0.0f; }
   }
-  acc.pg += m * pg;
-  acc.kl += m * kl;
-  acc.clip += (clipped && m != 0.0f) ? 1u : 0u;
-  acc.akl += m * (o - l);
-  acc.n += m != 0.0f ? 1u : 0u;
-  if (DLOGP) g = m * w * ((clipped ? 0.0f : -A * rho) + p.beta * dkl);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    bool on = ((mk >> (8 * k)) & 0xffu) != 0u;
+    if (!FULL) on = on && (t + k >= t0) && (t + k < t1);
+    const float m = on ? 1.0f : 0.0f;
+    const float l = f4_get(lv, k), o = f4_get(ov, k);
+    const float d = l - o;                    // log ratio
+    const float rho = exp2f(d * kLog2e);     // MUFU.EX2, ~2 ulp
+    float pg, clipf, A;
+    if (ADV == DFX_ADV_TOKEN) {
+      A = (f4_get(av, k) - mu) * rstd;        // mu = 0, rstd = 1 unless whitening
+      const float rc = fminf(fmaxf(rho, lo), hi);
+      const float pg1 = -A * rho, pg2 = -A * rc;
+      pg = fmaxf(pg1, pg2);
+      clipf = pg2 > pg1 ? 1.0f : 0.0f;
+    } else {
+      A = ua.A;
+      const float sr = ua.s * rho;
+      pg = ua.nA * fminf(sr, ua.sb);
+      clipf = sr > ua.sb ? 1.0f : 0.0f;
+    }
+    acc.pg = fmaf(m, pg, acc.pg);
+    acc.kl = fmaf(m, kl[k], acc.kl);
+    acc.akl = fmaf(-m, d, acc.akl);
+    acc.clip = fmaf(m, clipf, acc.clip);
+    acc.n += m;
+    aout[k] = on ? A : 0.0f;
+    if (DLOGP) gout[k] = m * w * ((clipf != 0.0f ? 0.0f : -A * rho) + p.beta * dkl[k]);
+  }
 }
 
 // Group stats with all lanes participating: lanes load the rewards in
@@ -208,23 +247,6 @@ __global__ void __launch_bounds__(256) grpo_adv_kernel(int64_t n_records, const 
   for (int32_t s = a + lane; s < b; s += 32) adv[s] = group_adv(__ldg(reward + s), g);
 }
 
-// Four tokens of one aligned vector. FULL: all four lie in [t0, t1).
-template <int ADV, bool DLOGP, bool FULL>
-__device__ __forceinline__ void loss_vec(const LossParams& p, float4 lv, float4 ov, float4 rv, float4 av, uint32_t mk,
-                                         int64_t t, int64_t t0, int64_t t1, float mu, float rstd, float w,
-                                         TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    bool on = ((mk >> (8 * k)) & 0xffu) != 0u;
-    if (!FULL) on = on && (t + k >= t0) && (t + k < t1);
-    const float m = on ? 1.0f : 0.0f;
-    float A = f4_get(av, k);
-    if (p.whiten) A = (A - mu) * rstd;
-    aout[k] = on ? A : 0.0f;
-    loss_token<ADV, DLOGP>(p, A, f4_get(lv, k), f4_get(ov, k), f4_get(rv, k), m, w, acc, gout[k]);
-  }
-}
-
 template <bool FULL>
 __device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, int64_t t1, const float (&v)[4]) {
   if (FULL) {
@@ -241,8 +263,8 @@ __device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, in
 // mask words, kUnroll vectors per lane in flight, fused advantage broadcast,
 // clipped surrogate, KL and masked partial sums in registers (f32 per round,
 // f64 across rounds), one deterministic warp reduction per slot.
-template <int ADV, bool ADV_OUT, bool DLOGP>
-__global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
+template <int ADV, int KL, bool DLOGP>
+__global__ void __launch_bounds__(256, 3) loss_slots_kernel(LossParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -292,6 +314,8 @@ __global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
     } else if (ADV == DFX_ADV_ROLLOUT) {
       A_unit = (float)__ldg(p.adv_roll_in + s);
     }
+    if (ADV != DFX_ADV_TOKEN) A_unit = (A_unit - mu) * rstd;  // identity unless whitening
+    const UnitAdv ua = unit_adv(A_unit, 1.0f - p.clip_lo, 1.0f + p.clip_hi);
     float w = 0.0f;
     if (DLOGP) {
       int gi = 0;
@@ -304,8 +328,7 @@ __global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
       else w = S > 0 ? (float)(1.0 / S) : 0.0f;
     }
 
-    double dpg = 0.0, dkl = 0.0, dakl = 0.0;
-    uint32_t dclip = 0, dn = 0;
+    double dpg = 0.0, dkl = 0.0, dakl = 0.0, dclip = 0.0, dn = 0.0;
     const int64_t vbeg = t0 >> 2;
     const int32_t nvec = (int32_t)(((t1 + 3) >> 2) - vbeg);
     const float* lp0 = p.lp + 4 * vbeg;
@@ -328,21 +351,22 @@ __global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
           if (ADV == DFX_ADV_TOKEN) av[j] = ldg_stream_f4(ad0 + 4 * i);
         }
       }
-      TokAcc acc{0.f, 0.f, 0.f, 0u, 0u};
+      TokAcc acc{0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j) {
         const int32_t i = ib + 32 * j;
         if (i >= nvec) break;
         const int64_t t = 4 * (vbeg + i);
-        if (ADV != DFX_ADV_TOKEN) av[j] = make_float4(A_unit, A_unit, A_unit, A_unit);
         float aout[4], gout[4];
         if (t >= t0 && t + 4 <= t1) {
-          loss_vec<ADV, DLOGP, true>(p, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout, gout);
-          if (ADV_OUT) store_vec<true>(p.adv_tok_out, t, t0, t1, aout);
+          loss_vec<ADV, KL, DLOGP, true>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
+                                         gout);
+          if (p.adv_tok_out) store_vec<true>(p.adv_tok_out, t, t0, t1, aout);
           if (DLOGP) store_vec<true>(p.dlogp, t, t0, t1, gout);
         } else {
-          loss_vec<ADV, DLOGP, false>(p, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout, gout);
-          if (ADV_OUT) store_vec<false>(p.adv_tok_out, t, t0, t1, aout);
+          loss_vec<ADV, KL, DLOGP, false>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
+                                          gout);
+          if (p.adv_tok_out) store_vec<false>(p.adv_tok_out, t, t0, t1, aout);
           if (DLOGP) store_vec<false>(p.dlogp, t, t0, t1, gout);
         }
       }
@@ -360,9 +384,9 @@ __global__ void __launch_bounds__(256, 4) loss_slots_kernel(LossParams p) {
     if (lane == 0) {
       part[u] = dpg;
       part[p.n_slots + u] = dkl;
-      part[2 * p.n_slots + u] = (double)dclip;
+      part[2 * p.n_slots + u] = dclip;
       part[3 * p.n_slots + u] = dakl;
-      part[4 * p.n_slots + u] = (double)dn;
+      part[4 * p.n_slots + u] = dn;
     }
   }
   // the last warp out restores the tickets for the next launch
@@ -580,7 +604,7 @@ SlotGeom geom_of(const dfx_packed* b, int64_t base) {
 }
 
 // persistent grid: as many 256-thread CTAs as fit on all SMs at once
-template <int ADV, bool AO, bool DL>
+template <int ADV, int KL, bool DL>
 void launch_slots(const LossParams& p, cudaStream_t st) {
   static thread_local int cached_dev = -1, cached_blocks = 0;
   int dev = 0;
@@ -588,21 +612,26 @@ void launch_slots(const LossParams& p, cudaStream_t st) {
   if (dev != cached_dev) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loss_slots_kernel<ADV, AO, DL>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loss_slots_kernel<ADV, KL, DL>, 256, 0);
     cached_blocks = sms * std::max(per_sm, 1);
     cached_dev = dev;
   }
-  loss_slots_kernel<ADV, AO, DL><<<cached_blocks, 256, 0, st>>>(p);
+  loss_slots_kernel<ADV, KL, DL><<<cached_blocks, 256, 0, st>>>(p);
+}
+
+template <int ADV, int KL>
+void launch_slots_kl(const LossParams& p, cudaStream_t st, bool dl) {
+  if (dl) launch_slots<ADV, KL, true>(p, st);
+  else launch_slots<ADV, KL, false>(p, st);
 }
 
 template <int ADV>
-void launch_slots_adv(const LossParams& p, cudaStream_t st, bool ao, bool dl) {
-  if (ao) {
-    if (dl) launch_slots<ADV, true, true>(p, st);
-    else launch_slots<ADV, true, false>(p, st);
-  } else {
-    if (dl) launch_slots<ADV, false, true>(p, st);
-    else launch_slots<ADV, false, false>(p, st);
+void launch_slots_adv(const LossParams& p, cudaStream_t st, int kl, bool dl) {
+  switch (kl) {
+    case DFX_KL_K1: launch_slots_kl<ADV, DFX_KL_K1>(p, st, dl); break;
+    case DFX_KL_K2: launch_slots_kl<ADV, DFX_KL_K2>(p, st, dl); break;
+    case DFX_KL_K3: launch_slots_kl<ADV, DFX_KL_K3>(p, st, dl); break;
+    default: launch_slots_kl<ADV, DFX_KL_NONE>(p, st, dl); break;
   }
 }
 
@@ -735,12 +764,11 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
   p.part = w.part;
   p.flags = args->flags;
   p.ticket = w.slot_ticket;
-  const bool ao = args->adv_tok_out != nullptr;
   if (args->ev_main_begin) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_begin), stream));
   switch (cfg->adv_source) {
-    case DFX_ADV_GROUP_FUSED: launch_slots_adv<DFX_ADV_GROUP_FUSED>(p, stream, ao, want_dl); break;
-    case DFX_ADV_ROLLOUT: launch_slots_adv<DFX_ADV_ROLLOUT>(p, stream, ao, want_dl); break;
-    default: launch_slots_adv<DFX_ADV_TOKEN>(p, stream, ao, want_dl); break;
+    case DFX_ADV_GROUP_FUSED: launch_slots_adv<DFX_ADV_GROUP_FUSED>(p, stream, cfg->kl_type, want_dl); break;
+    case DFX_ADV_ROLLOUT: launch_slots_adv<DFX_ADV_ROLLOUT>(p, stream, cfg->kl_type, want_dl); break;
+    default: launch_slots_adv<DFX_ADV_TOKEN>(p, stream, cfg->kl_type, want_dl); break;
   }
   DFX_LAUNCH_CHECK("loss_slots_kernel");
   if (args->ev_main_end) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_end), stream));
