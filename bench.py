@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--records", type=int, default=C2["records"])
+    ap.add_argument("--placement", default="box", choices=["box", "store"],
+                    help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
+                         "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")
     return ap.parse_args()
 
 
@@ -129,6 +132,59 @@ def ncu_traffic():
 
 
 # ---- the GPU arm ------------------------------------------------------------------------------------
+class DagSlice:
+    """group_advantage_compute (dp 8) -> DataBuffer put/get -> actor_train loss (dp 4, tp 2), box placement."""
+
+    STAGE = "group_advantage_compute"
+
+    def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box"):
+        self.dfx, self.ctx, self.it = dfx, ctx, 0
+        self.placement = placement
+        if placement == "box":
+            self.topo = Topology.box(8, world)
+            self.prod, self.cons = Layout(8, 1), Layout(4, 2)
+        else:
+            wpg = max(2, 8 // world)
+            self.topo = Topology.store_per_gpu(world, wpg)
+            self.prod, self.cons = Layout(world * wpg, 1), Layout(world * wpg // 2, 2)
+        meta = None
+        if world > 1:
+            import torch.distributed as dist
+            meta = dist.new_group(backend="gloo")  # host metadata side channel; token data moves over NCCL
+        self.store = Store(self.topo, rank, {self.STAGE: StagePlan(self.prod, self.cons)}, meta_group=meta)
+        self.local_p = [p for p in range(self.prod.dp) if self.topo.gpu_of_worker[p] == rank]
+        self.per = records // len(self.local_p)
+        self.world = world
+        from paper_2507_13833_b200.reshard import Plan
+        self.cross = Plan(self.topo, self.prod, self.cons, [self.per] * self.prod.dp, rank).cross
+        self.last = None
+
+    def step(self, batch, events=None):
+        dfx, ctx = self.dfx, self.ctx
+        dfx.fn_group_advantage(dfx.NodeSpec(self.STAGE), batch, ctx)
+        for j, p in enumerate(self.local_p):
+            self.store.put(self.STAGE, self.it, p, 0, batch.view_records(j * self.per, (j + 1) * self.per))
+        cb = self.store.ensure_ready(self.STAGE, self.it, self.cons)
+        res = dfx.ppo_loss(cb.batch, ctx, adv_source="rollout", loss_group_off=cb.roll_off, adv_tok_out=True,
+                           events=events)
+        for _ in self.store.local_workers:
+            self.store.worker_done(self.it)
+        self.it += 1
+        self.last = cb
+        return res, cb.batch
+
+    def launches_per_step(self):
+        # grpo_adv + loss_slots + finalize (+ pack, unpack and NCCL P2P when records cross GPUs)
+        return 3 + (3 if self.cross else 0)
+
+    def describe(self):
+        mode = ("zero-copy views: every consumer group's TP workers and producer groups share a GPU"
+                if not self.cross else "records cross GPUs over NVLink (grouped NCCL P2P) + pack/unpack kernels")
+        t = self.topo
+        return (f"{self.placement} placement B={t.num_nodes} W={t.workers_per_node}: dp{self.prod.dp}(tp1) -> "
+                f"dp{self.cons.dp}(tp2) over {self.world} GPU; {mode}")
+
+
 def run_dfx(args):
     import torch
     import torch.distributed as dist
@@ -147,7 +203,8 @@ def run_dfx(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2507_13833_b200.reshard import BoxReshard
+    from paper_2507_13833_b200.reshard import Layout, Topology
+    from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan
 
     L = _abi.lib()
     R, n = args.records, C2["n_roll"]
@@ -158,7 +215,7 @@ def run_dfx(args):
     ctx = dfx.StageContext()
     ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
     stream = torch.cuda.current_stream(dev)
-    resh = BoxReshard(world, rank, dev, producer_dp=8, consumer_dp=4)
+    resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement)
 
     ev0, ev1 = C.c_void_p(), C.c_void_p()
     _abi.check(L.dfx_event_create(C.byref(ev0)))
@@ -166,10 +223,7 @@ def run_dfx(args):
     kern_ms = []
 
     def step(time_kernel=False):
-        dfx.fn_group_advantage(dfx.NodeSpec("group_advantage_compute"), batch, ctx)
-        consumer, lgo = resh.exchange(batch, ctx)
-        res = dfx.ppo_loss(consumer, ctx, adv_source="rollout", loss_group_off=lgo, adv_tok_out=True,
-                           events=(ev0, ev1) if time_kernel else None)
+        res, consumer = resh.step(batch, events=(ev0, ev1) if time_kernel else None)
         if time_kernel:
             ms = C.c_float()
             _abi.check(L.dfx_event_elapsed_ms(ev0, ev1, C.byref(ms)))
@@ -188,7 +242,7 @@ def run_dfx(args):
     # the steady-state step is launch-bound at this size: capture it once in a CUDA graph when the
     # reshard has no host synchronization (all N <= 4 box placements)
     graph = None
-    if resh.local and not args.no_graph:
+    if not resh.cross and not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step()
@@ -250,13 +304,13 @@ def run_dfx(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 group stats/accumulators)",
             "data": "synthetic (keyed SplitMix64, generated on device; SURVEY.md §8(d))",
             "config": {"workload": f"C2 per GPU: {R} prompts x n={n} x UNIFORM[1,4096] tokens "
-                                   f"(~{tokens_local/1e6:.1f}M tokens/GPU), GRPO adv -> reshard dp8->dp4(tp2) "
-                                   f"box placement B=1 W=8 -> clipped loss + k3 KL token-mean",
+                                   f"(~{tokens_local/1e6:.1f}M tokens/GPU), GRPO adv -> DataBuffer reshard "
+                                   f"(dp_p -> dp_p/2, tp 2) -> clipped loss + k3 KL token-mean",
                        "tokens_per_gpu": tokens_local, "global_tokens": int(tokens_total),
                        "reshard": resh.describe(), "l2": "inputs (571 MB/GPU) larger than the 126 MB L2; no flush",
                        "parallelism": f"dp{world} (logical dp8->dp4 over {world} GPU)",
                        "cuda_graph": graph is not None},
-            "e2e": e2e, "gpu_launches": resh.launches_per_step + 3, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": resh.launches_per_step(), "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.result(),
         }
         print(json.dumps(line), flush=True)
@@ -280,7 +334,7 @@ def run_e2e(args, dfx, batch, ctx, resh, dev, stream, world):
                          {k: d[k] for k in ("lp", "old_lp", "ref_lp", "mask")},
                          host_group_off=batch.host_group_off, host_cu=batch.host_cu)
     h2d = sum(v.numel() * v.element_size() for v in h.values())
-    n_groups = 4
+    n_groups = len(resh.store.stages and resh.last.groups) if resh.last is not None else 1
     out_h = torch.empty(n_groups * 7, dtype=torch.float64).pin_memory()
     adv_h = torch.empty(batch.n_rollouts, dtype=torch.float64).pin_memory()
     d2h = out_h.numel() * 8 + adv_h.numel() * 8
@@ -288,9 +342,7 @@ def run_e2e(args, dfx, batch, ctx, resh, dev, stream, world):
     def e2e_step():
         for k in h:
             d[k].copy_(h[k], non_blocking=True)
-        dfx.fn_group_advantage(dfx.NodeSpec("group_advantage_compute"), eb, ctx)
-        consumer, lgo = resh.exchange(eb, ctx)
-        res = dfx.ppo_loss(consumer, ctx, adv_source="rollout", loss_group_off=lgo, adv_tok_out=True)
+        res, _ = resh.step(eb)
         out_h.copy_(res["out"].reshape(-1), non_blocking=True)
         adv_h.copy_(eb.channels["advantage"], non_blocking=True)
 

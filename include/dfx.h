@@ -183,6 +183,64 @@ dfx_status dfx_synth_tokens(uint64_t seed, const uint64_t* ids, int64_t n_record
                             uint8_t* mask, int32_t* token_id, dfx_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * DataBuffer reshard (DP m->n), replacing BufferStore::exchange/get
+ * (distflow/data_plane.hpp:237-442) and all_to_all (distflow/transport.hpp:718-754)
+ * for device-resident batches.
+ * ------------------------------------------------------------------------- */
+
+/* Host-only. The reference placement as an index list: for every consumer
+ * group d (dest-major) the records it receives, as indices into
+ * ordered = L_0 || ... || L_{dp_p-1} (L_p = producer group p's records).
+ * Errors: DFX_LAYOUT_ERROR (topology.hpp:53-68), DFX_INDIVISIBLE_ERROR
+ * (data_plane.hpp:414-416, :281-283). src_index may be NULL. */
+dfx_status dfx_reshard_placement(uint32_t num_nodes, uint32_t workers_per_node, uint32_t dp_p, uint32_t tp_p,
+                                 uint32_t dp_c, uint32_t tp_c, const uint64_t* group_counts,
+                                 uint64_t* dest_counts, uint64_t* src_index);
+
+/* One maximal run of consecutive records: producer group src_group's records
+ * [src_rec, src_rec+count) become consumer group dst_group's records
+ * [dst_rec, dst_rec+count). */
+typedef struct dfx_segment {
+  uint32_t dst_group;
+  uint32_t src_group;
+  uint64_t dst_rec;
+  uint64_t src_rec;
+  uint64_t count;
+} dfx_segment;
+
+/* Host-only. Writes up to cap segments (dest-major order) and returns the
+ * total count, or -status on a layout/divisibility error. */
+int64_t dfx_reshard_segments(uint32_t num_nodes, uint32_t workers_per_node, uint32_t dp_p, uint32_t tp_p,
+                             uint32_t dp_c, uint32_t tp_c, const uint64_t* group_counts, dfx_segment* out,
+                             int64_t cap);
+
+/* Device-side metadata of one segment: pointers at the slice start of the
+ * source arrays (a local producer batch, or a received pack buffer): ids
+ * [n_rec], group_off [n_rec+1] and cu_seqlens [n_roll+1] (source-absolute
+ * values), up to 4 f64 rollout channels [n_roll]; plus destination offsets
+ * (records, rollouts, absolute token index in the destination streams). */
+typedef struct dfx_seg_meta {
+  const uint64_t* ids;
+  const int32_t* group_off;
+  const int64_t* cu;
+  const double* ch[4];
+  int64_t n_rec, n_roll;
+  int64_t dst_rec, dst_roll, dst_tok;
+} dfx_seg_meta;
+
+/* Pack segments' metadata into contiguous send buffers (one CTA per segment):
+ * ids u64[n_rec] | cu i64[n_roll+1] | ch f64[n_ch][n_roll] | group_off i32[n_rec+1].
+ * segs_dev and out_dev are device arrays. */
+int64_t dfx_reshard_pack_bytes(int64_t n_rec, int64_t n_roll, int32_t n_ch);
+dfx_status dfx_reshard_pack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint8_t* const* out_dev,
+                            dfx_stream stream);
+/* Unpack into the destination batch, rebasing group_off / cu_seqlens and
+ * rebuilding roll_group. dst_ch_dev: device array of n_ch channel pointers. */
+dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint64_t* dst_ids,
+                              int32_t* dst_group_off, int32_t* dst_roll_group, int64_t* dst_cu,
+                              double* const* dst_ch_dev, dfx_stream stream);
+
+/* ---------------------------------------------------------------------------
  * Timing helpers (cudaEvent_t as void*), so ctypes callers can bracket a
  * kernel on the stream it runs on.
  * ------------------------------------------------------------------------- */

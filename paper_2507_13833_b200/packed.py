@@ -46,6 +46,8 @@ class PackedBatch:
     host_cu: np.ndarray | None = None
     meta_blob: np.ndarray | None = None            # host: per-record pre-serialized meta sections (optional)
     meta_off: np.ndarray | None = None
+    parent: "PackedBatch | None" = None            # views: the batch whose records [parent_rec, +n) this is
+    parent_rec: int = 0
 
     @property
     def device(self):
@@ -114,7 +116,17 @@ class PackedBatch:
         return b
 
     # ---- ABI view ------------------------------------------------------------------------
+    def _materialize(self) -> None:
+        """Views defer their rebased record metadata (group_off / roll_group) until a kernel needs it."""
+        if self.group_off is None:
+            dev = self.device
+            go = self.host_group_off
+            self.group_off = torch.from_numpy(go).to(dev, non_blocking=True)
+            self.roll_group = torch.from_numpy(np.repeat(np.arange(self.n_records, dtype=np.int32),
+                                                         np.diff(go))).to(dev, non_blocking=True)
+
     def struct(self) -> _abi.Packed:
+        self._materialize()
         s = self.streams
         ch = self.channels
         return _abi.Packed(self.n_records, self.n_rollouts, _ptr(self.group_off), _ptr(self.roll_group),
@@ -124,17 +136,16 @@ class PackedBatch:
 
     def view_records(self, r0: int, r1: int) -> "PackedBatch":
         """Zero-copy view of records [r0, r1): token streams and channels shared, record metadata rebased."""
+        if r0 == 0 and r1 == self.n_records:
+            return self
         go = self.host_group_off
         s0, s1 = int(go[r0]), int(go[r1])
         cu = self.host_cu[s0:s1 + 1]
         ngo = (go[r0:r1 + 1] - s0).astype(np.int32)
-        dev = self.device
-        v = PackedBatch(r1 - r0, s1 - s0, int(cu[0]), int(cu[-1] - cu[0]), self.ids[r0:r1],
-                        torch.from_numpy(ngo).to(dev, non_blocking=True),
-                        torch.from_numpy(np.repeat(np.arange(r1 - r0, dtype=np.int32), np.diff(ngo))).to(dev, non_blocking=True),
-                        self.cu_seqlens[s0:s1 + 1], {k: t[s0:s1] for k, t in self.channels.items()},
-                        dict(self.streams), host_group_off=ngo, host_cu=cu)
-        return v
+        root, base = (self.parent, self.parent_rec) if self.parent is not None else (self, 0)
+        return PackedBatch(r1 - r0, s1 - s0, int(cu[0]), int(cu[-1] - cu[0]), self.ids[r0:r1], None, None,
+                           self.cu_seqlens[s0:s1 + 1], {k: t[s0:s1] for k, t in self.channels.items()},
+                           dict(self.streams), host_group_off=ngo, host_cu=cu, parent=root, parent_rec=base + r0)
 
     def to_host(self) -> dict:
         """D2H of everything (tests / serialization)."""

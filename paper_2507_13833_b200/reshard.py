@@ -1,59 +1,387 @@
-"""DP m->n reshard of device-resident packed batches (distflow/data_plane.hpp BufferStore exchange/get).
+"""DataBuffer DP m->n reshard of device-resident packed batches.
 
-BoxReshard: the bench's placement -- one DataBuffer per box (B = 1, W = 8 logical workers), worker w on GPU
-w // (8 / P). Producer layout dp_p with tp 1, consumer layout dp_c with tp = 8 / dp_c.
-Destination group d receives (L_0 || ... || L_7)[d*G/dp_c, (d+1)*G/dp_c) (SURVEY.md App. A, B = 1), i.e. the
-producer groups [d*8/dp_c, (d+1)*8/dp_c). When every TP worker of d sits on the GPU that already holds those
-producer groups (P <= 8/tp_c... here P <= 4) the consumer batch is a zero-copy view of the producer batch.
+Replaces BufferStore::exchange/get (distflow/data_plane.hpp:296-442) and all_to_all (distflow/transport.hpp:718-754)
+for the GPU path. The reference placement is computed natively (dfx_reshard_segments, csrc/reshard.cu) as segments:
+runs of consecutive records of one producer group that land consecutively in one consumer group. Logical workers
+(the reference's B x W ranks) are mapped onto GPUs (one process per GPU); a producer group lives on the GPU of
+its TP-0 worker (only TP-0 puts, data_plane.hpp:245-248) and a consumer group is needed on every GPU hosting one
+of its TP workers (TP peers read identical batches, :266-292).
+
+Per exchange, on every rank (SPMD, all ranks call it for the same stage/iteration like ensure_ready):
+  1. sizes: rollout/token counts of every segment, filled by the owning rank from its host metadata and summed
+     over ranks (one small all-reduce; skipped on a single GPU);
+  2. a consumer batch holding this rank's consumer groups in dp order -- a zero-copy view when all of them are one
+     contiguous run of a local producer batch (every box placement with <= 4 GPUs), else freshly allocated;
+  3. token streams move as contiguous byte ranges: device copies when local, NCCL send/recv (grouped, one
+     ncclGroupStart/End) across GPUs over NVLink; record/rollout metadata moves as one packed buffer per
+     segment (dfx_reshard_pack) and is rebased into the consumer batch by dfx_reshard_unpack.
 """
 from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-from . import errors
+from . import _abi, errors
+from .packed import PackedBatch, padded_len
+
+CHANNELS = ("reward", "value", "advantage")
 
 
-class BoxReshard:
-    def __init__(self, world: int, rank: int, device, producer_dp: int = 8, consumer_dp: int = 4, workers: int = 8):
-        if workers % world:
-            raise errors.LayoutError(f"{workers} logical workers cannot be spread over {world} GPUs")
-        if workers % producer_dp or workers % consumer_dp:
-            raise errors.LayoutError("dp must divide the logical world")
-        self.world, self.rank, self.device = world, rank, torch.device(device)
-        self.W, self.dp_p, self.dp_c = workers, producer_dp, consumer_dp
-        self.tp_c = workers // consumer_dp
-        self.wpg = workers // world  # logical workers per GPU
-        self.local = self.tp_c <= self.wpg  # every consumer group's TP workers share this GPU
-        self._lgo_cache = {}
-        self.launches_per_step = 0 if self.local else 4
+class Segment(C.Structure):
+    _fields_ = [("dst_group", C.c_uint32), ("src_group", C.c_uint32), ("dst_rec", C.c_uint64),
+                ("src_rec", C.c_uint64), ("count", C.c_uint64)]
 
-    def describe(self) -> str:
-        mode = ("zero-copy views (all TP workers of each consumer group and its producer groups share a GPU)"
-                if self.local else "TP-partner exchange over NVLink (NCCL P2P) + metadata rebase")
-        return (f"B=1 W={self.W}: dp{self.dp_p}(tp1) -> dp{self.dp_c}(tp{self.tp_c}) over {self.world} GPU; {mode}")
 
-    def local_consumer_groups(self):
-        """Consumer DP groups with at least one TP worker on this GPU (dp_rank = worker // tp_c)."""
-        first_w, last_w = self.rank * self.wpg, (self.rank + 1) * self.wpg
-        return sorted({w // self.tp_c for w in range(first_w, last_w)})
+class SegMeta(C.Structure):
+    _fields_ = [("ids", C.c_void_p), ("group_off", C.c_void_p), ("cu", C.c_void_p), ("ch", C.c_void_p * 4),
+                ("n_rec", C.c_int64), ("n_roll", C.c_int64), ("dst_rec", C.c_int64), ("dst_roll", C.c_int64),
+                ("dst_tok", C.c_int64)]
 
-    def exchange(self, batch, ctx):
-        """Returns (consumer batch on this GPU, rollout offsets of its consumer groups)."""
-        if not self.local:
-            raise errors.Error("BoxReshard: cross-GPU exchange requires reshard.Reshard (general executor)")
-        groups = self.local_consumer_groups()
-        key = (id(batch.host_group_off), batch.n_records)
-        lgo = self._lgo_cache.get(key)
-        if lgo is None:
-            # producer groups on this GPU hold equal record counts; consumer group d = producer groups
-            # [d*pg, (d+1)*pg) with pg = dp_p/dp_c, all local here, in order
-            n_local_prod = self.dp_p // self.world
-            per_prod = batch.n_records // n_local_prod
-            per_cons = per_prod * (self.dp_p // self.dp_c)
-            rec_off = [i * per_cons for i in range(len(groups) + 1)]
-            if rec_off[-1] != batch.n_records:
-                raise errors.IndivisibleError.of("store holdings", batch.n_records, len(groups))
-            lgo = [int(batch.host_group_off[r]) for r in rec_off]
-            self._lgo_cache = {key: lgo}
-        return batch, lgo
+
+def _declare():
+    L = _abi.lib()
+    if getattr(L, "_reshard_declared", False):
+        return L
+    P = C.c_void_p
+    L.dfx_reshard_placement.argtypes = [C.c_uint32] * 6 + [P, P, P]
+    L.dfx_reshard_placement.restype = C.c_int32
+    L.dfx_reshard_segments.argtypes = [C.c_uint32] * 6 + [P, P, C.c_int64]
+    L.dfx_reshard_segments.restype = C.c_int64
+    L.dfx_reshard_pack_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
+    L.dfx_reshard_pack_bytes.restype = C.c_int64
+    L.dfx_reshard_pack.argtypes = [P, C.c_int32, C.c_int32, P, P]
+    L.dfx_reshard_pack.restype = C.c_int32
+    L.dfx_reshard_unpack.argtypes = [P, C.c_int32, C.c_int32, P, P, P, P, P, P]
+    L.dfx_reshard_unpack.restype = C.c_int32
+    L._reshard_declared = True
+    return L
+
+
+@dataclass(frozen=True)
+class Layout:
+    """distflow::ParallelLayout (topology.hpp:40-51)."""
+    dp: int
+    tp: int
+
+    def dp_rank(self, w: int) -> int:
+        return w // self.tp
+
+    def tp_rank(self, w: int) -> int:
+        return w % self.tp
+
+    def group_lead(self, d: int) -> int:
+        return d * self.tp
+
+
+@dataclass(frozen=True)
+class Topology:
+    """distflow::ClusterTopology (topology.hpp:11-35) plus the logical-worker -> GPU (process rank) mapping."""
+    num_nodes: int
+    workers_per_node: int
+    gpu_of_worker: tuple
+
+    @property
+    def world(self) -> int:
+        return self.num_nodes * self.workers_per_node
+
+    @staticmethod
+    def box(workers: int, n_gpus: int) -> "Topology":
+        """One DataBuffer per box (B = 1), W logical workers spread evenly over the GPUs."""
+        if workers % n_gpus:
+            raise errors.LayoutError(f"{workers} logical workers cannot be spread over {n_gpus} GPUs")
+        return Topology(1, workers, tuple(w // (workers // n_gpus) for w in range(workers)))
+
+    @staticmethod
+    def store_per_gpu(n_gpus: int, workers_per_gpu: int) -> "Topology":
+        """One DataBuffer per GPU (B = n_gpus, W = workers_per_gpu)."""
+        return Topology(n_gpus, workers_per_gpu,
+                        tuple(w // workers_per_gpu for w in range(n_gpus * workers_per_gpu)))
+
+
+def placement(topo: Topology, produced: Layout, consumed: Layout, group_counts):
+    """The reference's record placement: (dest_counts, src_index) -- see dfx_reshard_placement."""
+    L = _declare()
+    gc = np.ascontiguousarray(group_counts, np.uint64)
+    dc = np.zeros(consumed.dp, np.uint64)
+    idx = np.zeros(max(int(gc.sum()), 1), np.uint64)
+    _abi.check(L.dfx_reshard_placement(topo.num_nodes, topo.workers_per_node, produced.dp, produced.tp, consumed.dp,
+                                       consumed.tp, gc.ctypes.data, dc.ctypes.data, idx.ctypes.data))
+    return dc, idx[: int(gc.sum())]
+
+
+def segments(topo: Topology, produced: Layout, consumed: Layout, group_counts) -> list:
+    L = _declare()
+    gc = np.ascontiguousarray(group_counts, np.uint64)
+    args = (topo.num_nodes, topo.workers_per_node, produced.dp, produced.tp, consumed.dp, consumed.tp, gc.ctypes.data)
+    n = L.dfx_reshard_segments(*args, None, 0)
+    if n < 0:
+        _abi.check(int(-n))
+    buf = (Segment * max(n, 1))()
+    L.dfx_reshard_segments(*args, C.cast(buf, C.c_void_p), n)
+    return [(s.dst_group, s.src_group, s.dst_rec, s.src_rec, s.count) for s in buf[:n]]
+
+
+class Plan:
+    """Segments plus where every producer / consumer group lives."""
+
+    def __init__(self, topo: Topology, produced: Layout, consumed: Layout, group_counts, rank: int):
+        if len(topo.gpu_of_worker) != topo.world:
+            raise errors.LayoutError("gpu_of_worker must map every logical worker")
+        self.topo, self.produced, self.consumed, self.rank = topo, produced, consumed, rank
+        self.group_counts = np.asarray(group_counts, np.uint64)
+        self.segs = segments(topo, produced, consumed, group_counts)
+        self.src_rank = [topo.gpu_of_worker[produced.group_lead(p)] for p in range(produced.dp)]
+        self.dst_ranks = [sorted({topo.gpu_of_worker[consumed.group_lead(d) + t] for t in range(consumed.tp)})
+                          for d in range(consumed.dp)]
+        self.local_src = [p for p in range(produced.dp) if self.src_rank[p] == rank]
+        self.local_dst = [d for d in range(consumed.dp) if rank in self.dst_ranks[d]]
+        self.dest_counts = np.zeros(consumed.dp, np.int64)
+        for d, p, dr, sr, n in self.segs:
+            self.dest_counts[d] += n
+        # does any record cross GPUs? (box placements on <= 4 GPUs: never)
+        self.cross = any(self.src_rank[p] != r for d, p, _, _, _ in self.segs for r in self.dst_ranks[d])
+
+
+@dataclass
+class ConsumerBatch:
+    """This rank's consumer groups, concatenated in dp order, with per-group record/rollout offsets."""
+    batch: PackedBatch
+    groups: list            # consumer dp ranks held here, in order
+    rec_off: list           # record offsets per group (len(groups)+1)
+    roll_off: list          # rollout offsets per group
+    zero_copy: bool
+    bytes_sent: int = 0
+    bytes_recv: int = 0
+
+    def group_view(self, d: int) -> PackedBatch:
+        i = self.groups.index(d)
+        if self.rec_off[i] == 0 and self.rec_off[i + 1] == self.batch.n_records:
+            return self.batch
+        return self.batch.view_records(self.rec_off[i], self.rec_off[i + 1])
+
+    @property
+    def loss_group_off(self) -> list:
+        return list(self.roll_off)
+
+
+def _view_consistent(v: PackedBatch) -> bool:
+    """A view may be addressed through its parent only if every channel and stream it carries is still the
+    parent's storage (a stage function may have attached new channels to the view alone)."""
+    par = v.parent
+    s0 = int(par.host_group_off[v.parent_rec])
+    for c, t in v.channels.items():
+        pt = par.channels.get(c)
+        if pt is None or t.data_ptr() != pt.data_ptr() + s0 * pt.element_size():
+            return False
+    return set(v.streams) == set(par.streams) and all(v.streams[k] is par.streams[k] for k in v.streams)
+
+
+def _src_slices(plan: Plan, sources: dict):
+    """Per segment: (src batch, r0, r1, s0, s1, t0, t1) for locally held producer groups (host metadata)."""
+    out = {}
+    for i, (d, p, dr, sr, n) in enumerate(plan.segs):
+        if p not in sources:
+            continue
+        b, rbase = sources[p]
+        if b.parent is not None and _view_consistent(b):  # address the parent so contiguity is visible
+            b, rbase = b.parent, b.parent_rec + rbase
+        else:
+            b._materialize()
+        go, cu = b.host_group_off, b.host_cu
+        r0, r1 = rbase + int(sr), rbase + int(sr) + int(n)
+        s0, s1 = int(go[r0]), int(go[r1])
+        out[i] = (b, r0, r1, s0, s1, int(cu[s0]), int(cu[s1]))
+    return out
+
+
+def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, meta_group=None) -> ConsumerBatch:
+    """Run the reshard on this rank. sources: {producer dp rank: (PackedBatch, first record of that group in it)}
+    for every locally held producer group. schema: (stream name -> dtype, channel names), needed only on ranks
+    that hold no producer group. Collective across the ranks of `group` (torch.distributed, NCCL: token data) when
+    distributed; meta_group (gloo, CPU) carries the small size table without a device synchronisation."""
+    L = _declare()
+    rank = plan.rank
+    for p in plan.local_src:
+        if p not in sources:
+            raise errors.NotReadyError(f"producer group {p} has not been put on rank {rank}")
+    any_b = next(iter(sources.values()))[0] if sources else None
+    dev = any_b.device if any_b is not None else torch.device("cuda", torch.cuda.current_device())
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    if schema is None:
+        if any_b is None:
+            raise errors.Error("exchange on a rank without producer groups needs an explicit schema")
+        schema = ({k: v.dtype for k, v in any_b.streams.items()}, [c for c in CHANNELS if c in any_b.channels])
+    stream_specs, ch_names = schema
+    loc = _src_slices(plan, sources)
+
+    # 1. sizes of every segment (rollouts, tokens), filled by the owner, summed across ranks
+    nseg = len(plan.segs)
+    sizes = np.zeros((nseg, 2), np.int64)
+    for i, (b, r0, r1, s0, s1, t0, t1) in loc.items():
+        sizes[i] = (s1 - s0, t1 - t0)
+    if plan.cross and _distributed(group):
+        sizes = all_reduce_host(sizes, group, meta_group, dev)
+
+    # 2. consumer layout on this rank: its consumer groups in dp order
+    groups = plan.local_dst
+    seg_of = {d: [i for i, sg in enumerate(plan.segs) if sg[0] == d] for d in groups}
+    rec_off, roll_off, tok_off = [0], [0], [0]
+    dst = {}
+    for d in groups:
+        s_, t_ = roll_off[-1], tok_off[-1]
+        for i in seg_of[d]:
+            dst[i] = (rec_off[-1] + int(plan.segs[i][2]), s_, t_)
+            s_ += int(sizes[i, 0])
+            t_ += int(sizes[i, 1])
+        rec_off.append(rec_off[-1] + int(plan.dest_counts[d]))
+        roll_off.append(s_)
+        tok_off.append(t_)
+    order = [i for d in groups for i in seg_of[d]]
+
+    # zero-copy: every needed segment is local, from one batch, contiguous and in order
+    if order and all(i in loc for i in order):
+        b0 = loc[order[0]][0]
+        if all(loc[i][0] is b0 for i in order) and all(loc[order[k]][2] == loc[order[k + 1]][1]
+                                                       for k in range(len(order) - 1)):
+            r_a, r_b = loc[order[0]][1], loc[order[-1]][2]
+            view = b0 if (r_a == 0 and r_b == b0.n_records) else b0.view_records(r_a, r_b)
+            _, sent, recv_b = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)  # peers may need our groups
+            return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, recv_b)
+
+    # 3. allocate the consumer batch
+    R, S, T = rec_off[-1], roll_off[-1], tok_off[-1]
+    out = PackedBatch(R, S, 0, T, torch.empty(R, dtype=torch.int64, device=dev),
+                      torch.empty(R + 1, dtype=torch.int32, device=dev), torch.empty(S, dtype=torch.int32, device=dev),
+                      torch.empty(S + 1, dtype=torch.int64, device=dev),
+                      {c: torch.empty(S, dtype=torch.float64, device=dev) for c in ch_names},
+                      {k: torch.empty(padded_len(T), dtype=dt, device=dev) for k, dt in stream_specs.items()})
+    for t in out.streams.values():
+        t[T:].zero_()
+
+    metas = []
+    # local segments: token copies on this GPU + metadata straight from the source arrays
+    for i in order:
+        if i not in loc:
+            continue
+        b, r0, r1, s0, s1, t0, t1 = loc[i]
+        dr, ds, dt = dst[i]
+        for k, t in out.streams.items():
+            if t1 > t0:
+                t[dt:dt + (t1 - t0)].copy_(b.streams[k][t0:t1], non_blocking=True)
+        metas.append(_meta(b, r0, r1, s0, ch_names, dr, ds, dt))
+    # remote segments: one grouped NCCL P2P call (sends of our segments to peers, receives of theirs)
+    recvd, sent, recv_b = _p2p(plan, loc, sizes, dev, st, group, ch_names, (out, dst))
+    for i, buf in recvd:
+        n_rec, n_roll = int(plan.segs[i][4]), int(sizes[i, 0])
+        dr, ds, dt = dst[i]
+        base = buf.data_ptr()
+        m = SegMeta()
+        m.ids = base
+        m.cu = base + 8 * n_rec
+        for c in range(len(ch_names)):
+            m.ch[c] = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * c * n_roll
+        m.group_off = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * len(ch_names) * n_roll
+        m.n_rec, m.n_roll, m.dst_rec, m.dst_roll, m.dst_tok = n_rec, n_roll, dr, ds, dt
+        metas.append(m)
+    if metas:
+        seg_dev = _to_device((SegMeta * len(metas))(*metas), dev)
+        ch_dev = _to_device((C.c_void_p * max(1, len(ch_names)))(*[out.channels[c].data_ptr() for c in ch_names]), dev)
+        _abi.check(L.dfx_reshard_unpack(seg_dev.data_ptr(), len(metas), len(ch_names), out.ids.data_ptr(),
+                                        out.group_off.data_ptr(), out.roll_group.data_ptr(), out.cu_seqlens.data_ptr(),
+                                        ch_dev.data_ptr(), st.cuda_stream))
+        out._keep = [seg_dev, ch_dev, recvd]
+    # host metadata of the consumer batch (views and host-side checks need it)
+    out.host_group_off = out.group_off.cpu().numpy()
+    out.host_cu = out.cu_seqlens.cpu().numpy()
+    return ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
+
+
+def all_reduce_host(a: np.ndarray, group, meta_group, dev) -> np.ndarray:
+    """Sum a small int64 host table over ranks: over the CPU group when given, else through the device group."""
+    t = torch.from_numpy(np.ascontiguousarray(a, np.int64).reshape(-1).copy())
+    if meta_group is not None:
+        torch.distributed.all_reduce(t, group=meta_group)
+        return t.numpy().reshape(a.shape)
+    if torch.distributed.get_backend(group) == "nccl":
+        t = t.to(dev)
+    torch.distributed.all_reduce(t, group=group)
+    return t.cpu().numpy().reshape(a.shape)
+
+
+def _distributed(group) -> bool:
+    if not (torch.distributed.is_available() and torch.distributed.is_initialized()):
+        return False
+    return torch.distributed.get_world_size(group) > 1
+
+
+def _to_device(cstruct, dev) -> torch.Tensor:
+    """Small host table (ctypes array) -> device bytes (synchronous H2D: the table is freed right after)."""
+    return torch.frombuffer(bytearray(bytes(cstruct)), dtype=torch.uint8).to(dev)
+
+
+def _meta(b: PackedBatch, r0, r1, s0, ch_names, dr, ds, dt) -> SegMeta:
+    m = SegMeta()
+    m.ids = b.ids.data_ptr() + 8 * r0
+    m.group_off = b.group_off.data_ptr() + 4 * r0
+    m.cu = b.cu_seqlens.data_ptr() + 8 * s0
+    for c, name in enumerate(ch_names):
+        m.ch[c] = b.channels[name].data_ptr() + 8 * s0
+    m.n_rec, m.n_roll = r1 - r0, int(b.host_group_off[r1]) - s0
+    m.dst_rec, m.dst_roll, m.dst_tok = dr, ds, dt
+    return m
+
+
+def _p2p(plan: Plan, loc: dict, sizes, dev, st, group, ch_names, recv_into):
+    """Post every cross-GPU send of locally held segments and (when recv_into=(consumer batch, dst offsets) is
+    given) every receive of remote segments this rank needs, as ONE grouped NCCL call. Per (src, dst) pair the
+    messages are posted in segment order on both sides: packed metadata, then token streams sorted by name.
+    Returns ([(segment, packed metadata buffer)], bytes sent, bytes received)."""
+    if not plan.cross or not _distributed(group):
+        return [], 0, 0
+    L = _declare()
+    ops, recvd, to_pack = [], [], []
+    sent = recv_b = 0
+    me = plan.rank
+    for i, (d, p, dr, sr, n) in enumerate(plan.segs):
+        src = plan.src_rank[p]
+        for r in plan.dst_ranks[d]:
+            if src == me and r != me:
+                b, r0, r1, s0, s1, t0, t1 = loc[i]
+                nb = L.dfx_reshard_pack_bytes(r1 - r0, s1 - s0, len(ch_names))
+                buf = torch.empty(nb, dtype=torch.uint8, device=dev)
+                to_pack.append((_meta(b, r0, r1, s0, ch_names, 0, 0, 0), buf))
+                ops.append(torch.distributed.P2POp(torch.distributed.isend, buf, r, group))
+                sent += nb
+                for k in sorted(b.streams):
+                    sl = b.streams[k][t0:t1]
+                    if sl.numel():
+                        ops.append(torch.distributed.P2POp(torch.distributed.isend, sl, r, group))
+                        sent += sl.numel() * sl.element_size()
+            elif r == me and src != me and recv_into is not None:
+                out, dst = recv_into
+                dr_, ds, dt = dst[i]
+                n_tok = int(sizes[i, 1])
+                nb = L.dfx_reshard_pack_bytes(int(n), int(sizes[i, 0]), len(ch_names))
+                buf = torch.empty(nb, dtype=torch.uint8, device=dev)
+                recvd.append((i, buf))
+                ops.append(torch.distributed.P2POp(torch.distributed.irecv, buf, src, group))
+                recv_b += nb
+                for k in sorted(out.streams):
+                    sl = out.streams[k][dt:dt + n_tok]
+                    if sl.numel():
+                        ops.append(torch.distributed.P2POp(torch.distributed.irecv, sl, src, group))
+                        recv_b += sl.numel() * sl.element_size()
+    if to_pack:
+        seg_dev = _to_device((SegMeta * len(to_pack))(*[m for m, _ in to_pack]), dev)
+        out_dev = _to_device((C.c_void_p * len(to_pack))(*[b.data_ptr() for _, b in to_pack]), dev)
+        _abi.check(L.dfx_reshard_pack(seg_dev.data_ptr(), len(to_pack), len(ch_names), out_dev.data_ptr(),
+                                      st.cuda_stream))
+    if ops:
+        for w in torch.distributed.batch_isend_irecv(ops):
+            w.wait()
+    if to_pack:
+        st.synchronize()  # keep the pack tables alive until the sends completed
+    return recvd, sent, recv_b

@@ -1,0 +1,127 @@
+"""DeviceBufferStore: the reference BufferStore's contract (distflow/data_plane.hpp:225-457) over device batches.
+
+One instance per process (GPU). The logical workers it serves are the ones the topology maps to this GPU. The
+exchange itself is reshard.exchange (SPMD across GPUs). Kept from the reference, with its error types:
+  put        TP != 0 puts are suppressed and counted (:245-248); a producer group must be local (:249-254, "not
+             local to node" -> here "not local to rank"); a second put for the same group raises (:256-258);
+             iterations below the low-water mark raise StaleIterationError (:241-244)
+  get        runs ensure_ready, then returns the destination group's slice; TP peers on one GPU share one
+             zero-copy view of identical bytes (:266-292); a non-local destination raises
+  ensure_ready  once per (stage, iteration), when every local producer group has put; a missing put raises
+             NotReadyError naming the outstanding count (:340-344) -- a single-threaded rank cannot wait for it
+  worker_done   when every local logical worker reported, entries at or below the iteration are purged and the
+             low-water mark advances (:351-367)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import errors
+from .packed import PackedBatch
+from .reshard import ConsumerBatch, Layout, Plan, Topology, exchange
+
+
+@dataclass
+class StoreStagePlan:
+    """distflow::StoreStagePlan (data_plane.hpp:216-220)."""
+    produced: Layout
+    consumed: Layout | None = None
+
+
+@dataclass
+class _Entry:
+    by_group: dict = field(default_factory=dict)   # dp -> PackedBatch
+    ready: ConsumerBatch | None = None
+    consumed: Layout | None = None
+
+
+class DeviceBufferStore:
+    def __init__(self, topo: Topology, rank: int, stages: dict, group=None, stream=None, meta_group=None):
+        self.topo, self.rank, self.stages, self.group, self.stream = topo, rank, dict(stages), group, stream
+        self.meta_group = meta_group  # CPU (gloo) group for host metadata; data moves over `group` (NCCL)
+        self.local_workers = [w for w in range(topo.world) if topo.gpu_of_worker[w] == rank]
+        self._entries: dict = {}
+        self._done: dict = {}
+        self.low_water = 0
+        self.suppressed = 0
+        self.bytes_sent = 0
+        self.bytes_recv = 0
+
+    def _plan(self, stage: str) -> StoreStagePlan:
+        sp = self.stages.get(stage)
+        if sp is None:
+            raise errors.UnknownStageError(f"stage '{stage}' not in plan")
+        return sp
+
+    def _stale(self, what: str, iteration: int):
+        if iteration < self.low_water:
+            raise errors.StaleIterationError(f"{what} for iteration {iteration} below low water {self.low_water}")
+
+    def put(self, stage: str, iteration: int, dp_rank: int, tp_rank: int, batch: PackedBatch) -> bool:
+        sp = self._plan(stage)
+        self._stale("put", iteration)
+        if tp_rank != 0:
+            self.suppressed += 1
+            return False
+        if self.topo.gpu_of_worker[sp.produced.group_lead(dp_rank)] != self.rank:
+            raise errors.Error(f"put from dp group {dp_rank} not local to rank {self.rank}")
+        e = self._entries.setdefault((stage, iteration), _Entry())
+        if dp_rank in e.by_group:
+            raise errors.Error(f"duplicate put for stage '{stage}' group {dp_rank}")
+        e.by_group[dp_rank] = batch
+        return True
+
+    def ensure_ready(self, stage: str, iteration: int, fallback_to_layout: Layout) -> ConsumerBatch:
+        sp = self._plan(stage)
+        self._stale("get", iteration)
+        to = sp.consumed or fallback_to_layout
+        e = self._entries.setdefault((stage, iteration), _Entry())
+        if e.ready is not None:
+            return e.ready
+        local = [p for p in range(sp.produced.dp)
+                 if self.topo.gpu_of_worker[sp.produced.group_lead(p)] == self.rank]
+        missing = [p for p in local if p not in e.by_group]
+        if missing:
+            raise errors.NotReadyError(f"stage '{stage}' iteration {iteration} not ready: {len(missing)} puts "
+                                       "outstanding")
+        counts = [e.by_group[p].n_records if p in e.by_group else 0 for p in range(sp.produced.dp)]
+        # every rank must agree on the producer group sizes; ranks only know their own -> the plan needs them
+        counts = self._agree_counts(counts, local)
+        plan = Plan(self.topo, sp.produced, to, counts, self.rank)
+        sources = {p: (e.by_group[p], 0) for p in local}
+        e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group)
+        e.consumed = to
+        e.by_group = {}
+        self.bytes_sent += e.ready.bytes_sent
+        self.bytes_recv += e.ready.bytes_recv
+        return e.ready
+
+    def _agree_counts(self, counts, local):
+        """Producer group record counts are known only to their owners; every rank needs all of them."""
+        import numpy as np
+        import torch
+
+        from .reshard import _distributed, all_reduce_host
+        if not _distributed(self.group):
+            return counts
+        mine = np.array([c if p in local else 0 for p, c in enumerate(counts)], np.int64)
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        return all_reduce_host(mine, self.group, self.meta_group, dev).tolist()
+
+    def get(self, stage: str, iteration: int, dest_dp_rank: int, to_layout: Layout) -> PackedBatch:
+        ready = self.ensure_ready(stage, iteration, to_layout)
+        if dest_dp_rank not in ready.groups:
+            raise errors.Error(f"dp group {dest_dp_rank} not local to rank {self.rank}")
+        return ready.group_view(dest_dp_rank)
+
+    def worker_done(self, iteration: int) -> None:
+        c = self._done.get(iteration, 0) + 1
+        if c < len(self.local_workers):
+            self._done[iteration] = c
+            return
+        self._done.pop(iteration, None)
+        self.low_water = max(self.low_water, iteration + 1)
+        self._entries = {k: v for k, v in self._entries.items() if k[1] >= self.low_water}
+
+    def suppressed_count(self) -> int:
+        return self.suppressed
