@@ -63,8 +63,8 @@ def _declare(L):
     L.dfx_broadcast_advantage.argtypes = [C.POINTER(Packed), i64, i64, P, P, P]
     L.dfx_ppo_advantage.argtypes = [C.POINTER(Packed), P, P]
     L.dfx_gae_workspace_bytes.restype = sz
-    L.dfx_gae_workspace_bytes.argtypes = [i64]
-    L.dfx_gae.argtypes = [C.POINTER(Packed), f64, f64, P, P, P, P, sz, P]
+    L.dfx_gae_workspace_bytes.argtypes = [i64, i64]
+    L.dfx_gae.argtypes = [C.POINTER(Packed), i64, i64, f64, f64, P, P, P, P, sz, P]
     L.dfx_ppo_loss_workspace_bytes.restype = sz
     L.dfx_ppo_loss_workspace_bytes.argtypes = [i64, i64, i32]
     L.dfx_ppo_loss.argtypes = [C.POINTER(Packed), i64, i64, C.POINTER(LossCfg), C.POINTER(LossArgs), P, sz, P]

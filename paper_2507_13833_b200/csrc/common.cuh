@@ -67,6 +67,40 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// ---- TMA bulk copies + mbarriers (sm_90+ async proxy; SASS UBLKCP / SYNCS) ---------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completes on bar
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// order earlier generic-proxy shared-memory accesses before later async-proxy (TMA) writes
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---- reference hash (distflow/hash.hpp), integer-exact on device ------------
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -132,6 +166,14 @@ __device__ __forceinline__ bool slot_unit(const SlotGeom& g, int64_t u, int lane
   t0 = max(a, ws);
   t1 = min(b, ws + ((int64_t)1 << g.sh));
   return true;
+}
+
+// Host: window size of the streaming kernels. 2048-token windows: measured on
+// B200, shorter windows lose more to per-slot setup (search + reduction) than
+// they gain in balance, even for 4M-token batches.
+inline int slot_shift(int64_t token_span) {
+  (void)token_span;
+  return 11;
 }
 
 // Host: number of slots for n_seq rollouts spanning token_span tokens.

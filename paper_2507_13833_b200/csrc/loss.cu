@@ -555,7 +555,6 @@ using namespace dfx;
 
 namespace {
 
-constexpr int kSlotShift = 11;  // 2048-token windows
 constexpr int kWarpsPerBlock = 8;
 
 struct LossWs {
@@ -573,7 +572,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t span, int32_t n_groups) {
   LossWs w{};
-  const int64_t n_slots = slot_count(n_seq, span, kSlotShift);
+  const int64_t n_slots = slot_count(n_seq, span, slot_shift(span));
   w.nb = (int)std::max<int64_t>(1, (n_seq + kFinThreads * kFinSeqPerThread - 1) / (kFinThreads * kFinSeqPerThread));
   size_t off = 0;
   char* b = static_cast<char*>(base);
@@ -594,12 +593,12 @@ LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t span, int32_t n_groups)
   return w;
 }
 
-SlotGeom geom_of(const dfx_packed* b, int64_t base) {
+SlotGeom geom_of(const dfx_packed* b, int64_t base, int64_t span) {
   SlotGeom g;
   g.cu = b->cu_seqlens;
   g.n_seq = b->n_rollouts;
   g.base = base;
-  g.sh = kSlotShift;
+  g.sh = slot_shift(span);
   return g;
 }
 
@@ -653,8 +652,8 @@ dfx_status dfx_broadcast_advantage(const dfx_packed* b, int64_t token_base, int6
                                    const double* adv_roll, float* adv_tok, dfx_stream stream) {
   if (!b || !b->cu_seqlens || !b->mask || !adv_roll || !adv_tok) return fail(DFX_INVALID_ARGUMENT, "dfx_broadcast_advantage: null argument");
   if (b->n_rollouts <= 0) return DFX_OK;
-  const SlotGeom g = geom_of(b, token_base & ~int64_t(3));
-  const int64_t n_slots = slot_count(b->n_rollouts, token_span, kSlotShift);
+  const SlotGeom g = geom_of(b, token_base & ~int64_t(3), token_span);
+  const int64_t n_slots = slot_count(b->n_rollouts, token_span, slot_shift(token_span));
   broadcast_kernel<<<(unsigned)((n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, stream>>>(
       g, n_slots, adv_roll, b->mask, adv_tok);
   DFX_LAUNCH_CHECK("broadcast_kernel");
@@ -706,8 +705,8 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
   const int64_t S = b->n_rollouts;
   const LossWs w = loss_ws_layout(workspace, S, token_span, ng);
   if (!workspace || ws_bytes < w.bytes) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: workspace too small");
-  const SlotGeom g = geom_of(b, token_base & ~int64_t(3));
-  const int64_t n_slots = slot_count(S, token_span, kSlotShift);
+  const SlotGeom g = geom_of(b, token_base & ~int64_t(3), token_span);
+  const int64_t n_slots = slot_count(S, token_span, slot_shift(token_span));
   const bool want_dl = args->dlogp != nullptr;
 
   FinParams f{};

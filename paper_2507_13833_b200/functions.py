@@ -177,14 +177,15 @@ def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
     for n in ("token_reward", "value_tok", "mask"):
         _stream(batch, n)
     like = batch.streams["token_reward"]
-    adv = torch.zeros_like(like)
-    ret = torch.zeros_like(like)
+    adv = torch.empty_like(like)  # every token of the span is written
+    ret = torch.empty_like(like)
     wsum = torch.zeros(3, dtype=torch.float64, device=batch.device)
-    nbytes = _abi.lib().dfx_gae_workspace_bytes(batch.n_rollouts)
+    nbytes = _abi.lib().dfx_gae_workspace_bytes(batch.n_rollouts, batch.token_span)
     ws = ctx.workspace.get("gae", nbytes, batch.device)
     st = batch.struct()
-    _abi.check(_abi.lib().dfx_gae(C.byref(st), float(ctx.gae_gamma), float(ctx.gae_lambda), _ptr(adv), _ptr(ret),
-                                  _ptr(wsum), _ptr(ws), ws.numel(), ctx.cuda_stream(batch.device)))
+    _abi.check(_abi.lib().dfx_gae(C.byref(st), batch.token_base, batch.token_span, float(ctx.gae_gamma),
+                                  float(ctx.gae_lambda), _ptr(adv), _ptr(ret), _ptr(wsum), _ptr(ws), ws.numel(),
+                                  ctx.cuda_stream(batch.device)))
     batch.streams["advantage"] = adv
     batch.streams["returns"] = ret
     batch.channels["_whiten_sums"] = wsum

@@ -1,0 +1,146 @@
+"""Per-config kernel timings (CUDA events, warm, inputs resident in HBM) for BASELINE.json's configs.
+
+usage: python tools/measure_configs.py [--out profiles/r01_configs.json]
+C1 GRPO 64x8x1024 dense; C2 GRPO 1024x16xU[1,4096]; C3 PPO 512x8192 (GAE + whitening + clipped loss);
+C5 GRPO per-GPU share of 4096x16 skewed <=16k at 8 GPUs (512 prompts); C4 reshard 16.8M tokens dp8->dp4->dp8
+on one GPU (logical workers; zero-copy) -- the multi-GPU reshard is measured by bench.py --gpus N.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2507_13833_b200 as dfx  # noqa: E402
+from paper_2507_13833_b200 import _abi  # noqa: E402
+
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"]
+
+
+def timeit(fn, iters=30, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def kernel_ms(fn_with_events, iters=20):
+    L = _abi.lib()
+    e0, e1 = C.c_void_p(), C.c_void_p()
+    L.dfx_event_create(C.byref(e0))
+    L.dfx_event_create(C.byref(e1))
+    out = []
+    for i in range(iters + 3):
+        fn_with_events((e0, e1))
+        ms = C.c_float()
+        L.dfx_event_elapsed_ms(e0, e1, C.byref(ms))
+        if i >= 3:
+            out.append(ms.value)
+    out.sort()
+    return out[len(out) // 2]
+
+
+def grpo(name, R, n, dist, streams=("lp", "old_lp", "ref_lp", "mask")):
+    b = dfx.PackedBatch.synthetic(1, R, n, dist, streams=streams)
+    ctx = dfx.StageContext()
+    T = b.token_span
+    bytes_ = T * 17 + b.n_rollouts * 16
+    step = lambda: dfx.ppo_loss(b, ctx, adv_source="group", adv_tok_out=True)  # noqa: E731
+    ms = timeit(step)
+    km = kernel_ms(lambda ev: dfx.ppo_loss(b, ctx, adv_source="group", adv_tok_out=True, events=ev))
+    return {"config": name, "tokens": T, "rollouts": b.n_rollouts, "step_ms": ms, "kernel_ms": km,
+            "tokens_per_s": T / (ms / 1e3), "kernel_gbs": bytes_ / (km / 1e3) / 1e9,
+            "kernel_frac_of_hbm": bytes_ / (km / 1e3) / 1e9 / PEAK, "bytes_per_launch": bytes_,
+            "step": "fused GRPO group stats + broadcast + clipped surrogate + k3 KL (+adv write)"}
+
+
+def ppo_c3():
+    b = dfx.PackedBatch.synthetic(1, 512, 1, dfx.TokenDist("constant", 8192),
+                                  streams=("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward"))
+    ctx = dfx.StageContext(gae_gamma=1.0, gae_lambda=0.95)
+    ctx.loss = dfx.LossConfig(whiten=True)
+    T = b.token_span
+    node = dfx.NodeSpec("gae")
+
+    def step():
+        dfx.fn_gae_advantage(node, b, ctx)
+        dfx.ppo_loss(b, ctx, adv_source="token")
+
+    ms = timeit(step)
+    g_ms = timeit(lambda: dfx.fn_gae_advantage(node, b, ctx))
+    km = kernel_ms(lambda ev: dfx.ppo_loss(b, ctx, adv_source="token", events=ev))
+    gae_bytes = T * 17
+    loss_bytes = T * 17
+    return {"config": "C3", "tokens": T, "step_ms": ms, "tokens_per_s": T / (ms / 1e3),
+            "gae_ms": g_ms, "gae_gbs": gae_bytes / (g_ms / 1e3) / 1e9,
+            "gae_frac_of_hbm": gae_bytes / (g_ms / 1e3) / 1e9 / PEAK,
+            "loss_kernel_ms": km, "loss_gbs": loss_bytes / (km / 1e3) / 1e9,
+            "loss_frac_of_hbm": loss_bytes / (km / 1e3) / 1e9 / PEAK,
+            "step_frac_of_hbm": (gae_bytes + loss_bytes) / (ms / 1e3) / 1e9 / PEAK,
+            "step": "GAE reverse scan (+whitening sums) -> whitened clipped surrogate + k3 KL token-mean"}
+
+
+def reshard_c4():
+    from paper_2507_13833_b200.reshard import Layout, Topology
+    from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan
+    b = dfx.PackedBatch.synthetic(11, 1024, 16, dfx.TokenDist("constant", 1024),
+                                  streams=("token_id", "lp", "old_lp", "ref_lp"))
+    ctx = dfx.StageContext()
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
+    res = {}
+    for name, topo in {"box_B1_W8": Topology.box(8, 1), "store_B2_W4": Topology(2, 4, (0,) * 8),
+                       "store_B4_W2": Topology(4, 2, (0,) * 8)}.items():
+        st = DeviceBufferStore(topo, 0, {"s": StoreStagePlan(Layout(8, 1), Layout(4, 2)),
+                                         "t": StoreStagePlan(Layout(4, 2), Layout(8, 1))})
+        it = [0]
+
+        def rt():
+            i = it[0]
+            for p in range(8):
+                st.put("s", i, p, 0, b.view_records(128 * p, 128 * (p + 1)))
+            cb = st.ensure_ready("s", i, Layout(4, 2))
+            for d in range(4):
+                st.put("t", i, d, 0, cb.group_view(d))
+                st.put("t", i, d, 1, cb.group_view(d))
+            st.ensure_ready("t", i, Layout(8, 1))
+            for _ in range(8):
+                st.worker_done(i)
+            it[0] += 1
+        ms = timeit(rt, iters=10, warm=2)
+        res[name] = {"round_trip_ms": ms, "tokens_per_s": b.token_span / (ms / 1e3),
+                     "moved_bytes_per_trip": 0 if name.startswith("box") else 2 * b.token_span * 16}
+    return {"config": "C4 (1 GPU, 8 logical workers)", "tokens": b.token_span, "payload_bytes_per_token": 16,
+            "placements": res}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    rows = [grpo("C1", 64, 8, dfx.TokenDist("constant", 1024)),
+            grpo("C2", 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096)),
+            ppo_c3(),
+            grpo("C5/8 (one GPU's share: 512 prompts)", 512, 16, dfx.TokenDist("skewed", 0, 1, 16384)),
+            reshard_c4()]
+    for r in rows:
+        print(json.dumps(r), flush=True)
+    if a.out:
+        json.dump({"peak_hbm_gbs": PEAK, "gpu": torch.cuda.get_device_name(), "rows": rows}, open(a.out, "w"),
+                  indent=1)
+
+
+if __name__ == "__main__":
+    main()
