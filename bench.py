@@ -122,13 +122,19 @@ def measured_peak_hbm():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture, if present."""
-    p = os.path.join(ROOT, "profiles", "ncu_loss_slots.json")
-    try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:  # noqa: BLE001
-        return None
+    """dram bytes per launch of the dominant kernel from the newest committed ncu --set full capture
+    (profiles/*loss_slots*.json, written by tools/ncu_summary.py from a capture of the same C2 step)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*loss_slots*.json")), key=os.path.getmtime)
+    for p in reversed(files):
+        try:
+            with open(p) as f:
+                v = json.load(f).get("dram_bytes_per_launch")
+            if v:
+                return v
+        except Exception:  # noqa: BLE001
+            continue
+    return None
 
 
 # ---- the GPU arm ------------------------------------------------------------------------------------

@@ -229,9 +229,11 @@ __global__ void __launch_bounds__(kGaeThreads, 2) gae_kernel(GaeParams p) {
       Aff tot{0.0, 1.0};
       for (int w = kGaeThreads / 32 - 1; w >= 0; --w) tot = compose(s_warp[w], tot);
       double X = 0.0;
-      // a tile containing a rollout end has c == 0: its value does not depend on the tiles to its right
-      if (tile < p.n_tiles - 1 && tot.c != 0.0) {
-        if (lane == 0) rec_store(p.rec + tile, tot.d, (float)tot.c, F_AGG);
+      // A tile containing a rollout end has c == 0: its inclusive value does not depend on the tiles to its
+      // right, so it is published at once (tiles to the left stop their look-back here). The carry X is still
+      // resolved below: tokens after the tile's last rollout end need it.
+      if (lane == 0) rec_store(p.rec + tile, tot.d, (float)tot.c, tot.c == 0.0 ? F_INC : F_AGG);
+      if (tile < p.n_tiles - 1) {
         Aff G{0.0, 1.0};
         for (int64_t j0 = tile + 1;; j0 += 32) {
           const int64_t j = j0 + lane;
