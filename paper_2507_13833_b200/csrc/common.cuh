@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/dfx.h"
@@ -173,7 +174,12 @@ __device__ __forceinline__ bool slot_unit(const SlotGeom& g, int64_t u, int lane
 // they gain in balance, even for 4M-token batches.
 inline int slot_shift(int64_t token_span) {
   (void)token_span;
-  return 11;
+  static const int sh = [] {
+    const char* e = std::getenv("DFX_SLOT_SHIFT");  // tuning knob (benchmarking only)
+    const int v = e ? std::atoi(e) : 11;
+    return v >= 8 && v <= 14 ? v : 11;
+  }();
+  return sh;
 }
 
 // Host: number of slots for n_seq rollouts spanning token_span tokens.

@@ -6,6 +6,8 @@
 // :163-172 (fn_ppo_advantage), :176-182 (fn_train slot the loss fills).
 // HBM-bound streaming kernels: no tensor cores (no dense contraction).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -263,8 +265,8 @@ __device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, in
 // mask words, kUnroll vectors per lane in flight, fused advantage broadcast,
 // clipped surrogate, KL and masked partial sums in registers (f32 per round,
 // f64 across rounds), one deterministic warp reduction per slot.
-template <int ADV, int KL, bool DLOGP>
-__global__ void __launch_bounds__(256, 3) loss_slots_kernel(LossParams p) {
+template <int ADV, int KL, bool DLOGP, int UNROLL = 2, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(256, 3) loss_slots_kernel(LossParams p) {
     const float* rf0 = p.ref_lp + 4 * vbeg;
     const uint8_t* mk0 = p.mask + 4 * vbeg;
     const float* ad0 = ADV == DFX_ADV_TOKEN ? p.adv_tok_in + 4 * vbeg : nullptr;
-    constexpr int kUnroll = 2;
+    constexpr int kUnroll = UNROLL;
     for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
       float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
       uint32_t mk[kUnroll];
@@ -603,19 +605,46 @@ SlotGeom geom_of(const dfx_packed* b, int64_t base, int64_t span) {
 }
 
 // persistent grid: as many 256-thread CTAs as fit on all SMs at once
-template <int ADV, int KL, bool DL>
-void launch_slots(const LossParams& p, cudaStream_t st) {
+template <int ADV, int KL, bool DL, int U, int MB>
+void launch_variant(const LossParams& p, cudaStream_t st) {
   static thread_local int cached_dev = -1, cached_blocks = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev != cached_dev) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loss_slots_kernel<ADV, KL, DL>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loss_slots_kernel<ADV, KL, DL, U, MB>, 256, 0);
     cached_blocks = sms * std::max(per_sm, 1);
     cached_dev = dev;
   }
-  loss_slots_kernel<ADV, KL, DL><<<cached_blocks, 256, 0, st>>>(p);
+  loss_slots_kernel<ADV, KL, DL, U, MB><<<cached_blocks, 256, 0, st>>>(p);
+}
+
+// Tuning knob (benchmarking only): DFX_LOSS_VARIANT=u2b3 (default) | u3b2 | u4b2 | u2b2 selects the
+// unroll depth (vectors in flight per lane) and the CTAs-per-SM register budget of the hot configuration.
+inline int loss_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("DFX_LOSS_VARIANT");
+    if (!e) return 0;
+    const std::string s(e);
+    return s == "u3b2" ? 1 : s == "u4b2" ? 2 : s == "u2b2" ? 3 : s == "u1b4" ? 4 : s == "u2b4" ? 5 : 0;
+  }();
+  return v;
+}
+
+template <int ADV, int KL, bool DL>
+void launch_slots(const LossParams& p, cudaStream_t st) {
+  if (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL) {
+    switch (loss_variant()) {
+      case 1: return launch_variant<ADV, KL, DL, 3, 2>(p, st);
+      case 2: return launch_variant<ADV, KL, DL, 4, 2>(p, st);
+      case 3: return launch_variant<ADV, KL, DL, 2, 2>(p, st);
+      case 4: return launch_variant<ADV, KL, DL, 1, 4>(p, st);
+      case 5: return launch_variant<ADV, KL, DL, 2, 4>(p, st);
+      default: break;
+    }
+  }
+  launch_variant<ADV, KL, DL, 2, 3>(p, st);
 }
 
 template <int ADV, int KL>
