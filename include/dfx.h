@@ -233,15 +233,28 @@ typedef struct dfx_seg_meta {
 
 /* Pack segments' metadata into contiguous send buffers (one CTA per segment):
  * ids u64[n_rec] | cu i64[n_roll+1] | ch f64[n_ch][n_roll] | group_off i32[n_rec+1].
- * segs_dev and out_dev are device arrays. */
+ * segs and out are HOST arrays (the table travels in the kernel parameters);
+ * the pointers inside may be device or peer-mapped addresses. n_ch <= 4. */
 int64_t dfx_reshard_pack_bytes(int64_t n_rec, int64_t n_roll, int32_t n_ch);
-dfx_status dfx_reshard_pack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint8_t* const* out_dev,
+dfx_status dfx_reshard_pack(const dfx_seg_meta* segs, int32_t n_segs, int32_t n_ch, uint8_t* const* out,
                             dfx_stream stream);
 /* Unpack into the destination batch, rebasing group_off / cu_seqlens and
- * rebuilding roll_group. dst_ch_dev: device array of n_ch channel pointers. */
-dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint64_t* dst_ids,
+ * rebuilding roll_group. segs and dst_ch are HOST arrays (n_ch <= 4 channel
+ * pointers into the destination). */
+dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs, int32_t n_segs, int32_t n_ch, uint64_t* dst_ids,
                               int32_t* dst_group_off, int32_t* dst_roll_group, int64_t* dst_cu,
-                              double* const* dst_ch_dev, dfx_stream stream);
+                              double* const* dst_ch, dfx_stream stream);
+
+/* Peer memory for the NVLink pull transport. dfx_ipc_export returns the IPC
+ * handle of the allocation containing ptr and ptr's offset in it; a peer maps
+ * it with dfx_ipc_open. Map a peer process's allocation
+ * (cudaIpcMemHandle_t bytes, handle_bytes == 64) into the CURRENT device's
+ * context with lazy peer access, cached per (device, handle) -- no context is
+ * created on the peer device. dfx_copy_async is cudaMemcpyAsync(Default) so
+ * peer-mapped sources copy over NVLink on the caller's stream. */
+dfx_status dfx_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, uint64_t* offset_out);
+dfx_status dfx_ipc_open(const void* handle, size_t handle_bytes, void** base);
+dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream stream);
 
 /* ---------------------------------------------------------------------------
  * Timing helpers (cudaEvent_t as void*), so ctypes callers can bracket a

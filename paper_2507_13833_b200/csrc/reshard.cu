@@ -78,11 +78,21 @@ dfx_status placement(uint32_t B, uint32_t W, uint32_t dp_p, uint32_t tp_p, uint3
 }  // namespace
 
 // ---- metadata pack / unpack --------------------------------------------------------------
-// One CTA per segment. Unpack rebases: dst_go[dr+i] = go[i]-go[0]+droll ; dst_cu[droll+j] = cu[j]-cu[0]+dtok ;
-// roll_group[droll+j] = dr + (record of rollout j) ; ids / channels copied.
-__global__ void unpack_kernel(const dfx_seg_meta* __restrict__ segs, int n_ch, uint64_t* dst_ids, int32_t* dst_go,
-                              int32_t* dst_rg, int64_t* dst_cu, double* const* dst_ch) {
-  const dfx_seg_meta& m = segs[blockIdx.x];
+// One CTA per segment; the segment table travels by value in the kernel parameters (no H2D copy, no host sync).
+// Unpack rebases: dst_go[dr+i] = go[i]-go[0]+droll ; dst_cu[droll+j] = cu[j]-cu[0]+dtok ;
+// roll_group[droll+j] = dr + (record of rollout j) ; ids / channels copied. Source pointers may be peer-mapped
+// (NVLink pull transport): the kernel then reads the producer GPU's metadata directly.
+constexpr int kSegsPerLaunch = 48;
+struct SegBatch {
+  dfx_seg_meta seg[kSegsPerLaunch];
+  double* dst_ch[4];
+  uint8_t* out[kSegsPerLaunch];
+};
+
+__global__ void unpack_kernel(const SegBatch sb, int n_ch, uint64_t* dst_ids, int32_t* dst_go, int32_t* dst_rg,
+                              int64_t* dst_cu) {
+  const dfx_seg_meta& m = sb.seg[blockIdx.x];
+  double* const* dst_ch = sb.dst_ch;
   const int64_t g0 = m.group_off[0], c0 = m.cu[0];
   for (int64_t i = threadIdx.x; i <= m.n_rec; i += blockDim.x) {
     const int64_t gi = m.group_off[i];
@@ -102,9 +112,9 @@ __global__ void unpack_kernel(const dfx_seg_meta* __restrict__ segs, int n_ch, u
 
 // Pack: gather one segment's metadata into a contiguous buffer laid out as
 //   ids u64[n_rec] | cu i64[n_roll+1] | ch f64[n_ch][n_roll] | group_off i32[n_rec+1]
-__global__ void pack_kernel(const dfx_seg_meta* __restrict__ segs, int n_ch, uint8_t* const* out) {
-  const dfx_seg_meta& m = segs[blockIdx.x];
-  uint8_t* o = out[blockIdx.x];
+__global__ void pack_kernel(const SegBatch sb, int n_ch) {
+  const dfx_seg_meta& m = sb.seg[blockIdx.x];
+  uint8_t* o = sb.out[blockIdx.x];
   uint64_t* ids = reinterpret_cast<uint64_t*>(o);
   int64_t* cu = reinterpret_cast<int64_t*>(ids + m.n_rec);
   double* ch = reinterpret_cast<double*>(cu + m.n_roll + 1);
@@ -166,23 +176,37 @@ int64_t dfx_reshard_segments(uint32_t B, uint32_t W, uint32_t dp_p, uint32_t tp_
   return n;
 }
 
-dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint64_t* dst_ids,
+dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs, int32_t n_segs, int32_t n_ch, uint64_t* dst_ids,
                               int32_t* dst_group_off, int32_t* dst_roll_group, int64_t* dst_cu,
-                              double* const* dst_ch_dev, dfx_stream stream) {
+                              double* const* dst_ch, dfx_stream stream) {
   if (n_segs <= 0) return DFX_OK;
-  if (!segs_dev || !dst_ids || !dst_group_off || !dst_roll_group || !dst_cu || (n_ch > 0 && !dst_ch_dev))
-    return fail(DFX_INVALID_ARGUMENT, "dfx_reshard_unpack: null argument");
-  unpack_kernel<<<n_segs, 256, 0, stream>>>(segs_dev, n_ch, dst_ids, dst_group_off, dst_roll_group, dst_cu, dst_ch_dev);
-  DFX_LAUNCH_CHECK("unpack_kernel");
+  if (!segs || !dst_ids || !dst_group_off || !dst_roll_group || !dst_cu || (n_ch > 0 && !dst_ch) || n_ch > 4)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_reshard_unpack: bad argument");
+  for (int32_t s0 = 0; s0 < n_segs; s0 += kSegsPerLaunch) {
+    const int32_t n = std::min<int32_t>(kSegsPerLaunch, n_segs - s0);
+    SegBatch sb{};
+    for (int32_t i = 0; i < n; ++i) sb.seg[i] = segs[s0 + i];
+    for (int32_t c = 0; c < n_ch; ++c) sb.dst_ch[c] = dst_ch[c];
+    unpack_kernel<<<n, 256, 0, stream>>>(sb, n_ch, dst_ids, dst_group_off, dst_roll_group, dst_cu);
+    DFX_LAUNCH_CHECK("unpack_kernel");
+  }
   return DFX_OK;
 }
 
-dfx_status dfx_reshard_pack(const dfx_seg_meta* segs_dev, int32_t n_segs, int32_t n_ch, uint8_t* const* out_dev,
+dfx_status dfx_reshard_pack(const dfx_seg_meta* segs, int32_t n_segs, int32_t n_ch, uint8_t* const* out,
                             dfx_stream stream) {
   if (n_segs <= 0) return DFX_OK;
-  if (!segs_dev || !out_dev) return fail(DFX_INVALID_ARGUMENT, "dfx_reshard_pack: null argument");
-  pack_kernel<<<n_segs, 256, 0, stream>>>(segs_dev, n_ch, out_dev);
-  DFX_LAUNCH_CHECK("pack_kernel");
+  if (!segs || !out || n_ch > 4) return fail(DFX_INVALID_ARGUMENT, "dfx_reshard_pack: bad argument");
+  for (int32_t s0 = 0; s0 < n_segs; s0 += kSegsPerLaunch) {
+    const int32_t n = std::min<int32_t>(kSegsPerLaunch, n_segs - s0);
+    SegBatch sb{};
+    for (int32_t i = 0; i < n; ++i) {
+      sb.seg[i] = segs[s0 + i];
+      sb.out[i] = out[s0 + i];
+    }
+    pack_kernel<<<n, 256, 0, stream>>>(sb, n_ch);
+    DFX_LAUNCH_CHECK("pack_kernel");
+  }
   return DFX_OK;
 }
 

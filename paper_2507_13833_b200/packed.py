@@ -116,6 +116,13 @@ class PackedBatch:
         return b
 
     # ---- ABI view ------------------------------------------------------------------------
+    def ensure_host_meta(self) -> None:
+        """Batches produced on the device (e.g. by a reshard) fetch their host offsets lazily, only when a host
+        consumer (views, the reshard planner) needs them."""
+        if self.host_group_off is None and self.group_off is not None:
+            self.host_group_off = self.group_off.cpu().numpy()
+            self.host_cu = self.cu_seqlens.cpu().numpy()
+
     def _materialize(self) -> None:
         """Views defer their rebased record metadata (group_off / roll_group) until a kernel needs it."""
         if self.group_off is None:
@@ -138,6 +145,7 @@ class PackedBatch:
         """Zero-copy view of records [r0, r1): token streams and channels shared, record metadata rebased."""
         if r0 == 0 and r1 == self.n_records:
             return self
+        self.ensure_host_meta()
         go = self.host_group_off
         s0, s1 = int(go[r0]), int(go[r1])
         cu = self.host_cu[s0:s1 + 1]

@@ -70,6 +70,12 @@ def _declare():
     L.dfx_reshard_pack.restype = C.c_int32
     L.dfx_reshard_unpack.argtypes = [P, C.c_int32, C.c_int32, P, P, P, P, P, P]
     L.dfx_reshard_unpack.restype = C.c_int32
+    L.dfx_ipc_export.argtypes = [P, P, C.POINTER(C.c_uint64)]
+    L.dfx_ipc_export.restype = C.c_int32
+    L.dfx_ipc_open.argtypes = [P, C.c_size_t, C.POINTER(C.c_void_p)]
+    L.dfx_ipc_open.restype = C.c_int32
+    L.dfx_copy_async.argtypes = [P, P, C.c_size_t, P]
+    L.dfx_copy_async.restype = C.c_int32
     L._reshard_declared = True
     return L
 
@@ -204,6 +210,7 @@ def _src_slices(plan: Plan, sources: dict):
             b, rbase = b.parent, b.parent_rec + rbase
         else:
             b._materialize()
+        b.ensure_host_meta()
         go, cu = b.host_group_off, b.host_cu
         r0, r1 = rbase + int(sr), rbase + int(sr) + int(n)
         s0, s1 = int(go[r0]), int(go[r1])
@@ -211,11 +218,17 @@ def _src_slices(plan: Plan, sources: dict):
     return out
 
 
-def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, meta_group=None) -> ConsumerBatch:
+def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, meta_group=None,
+             transport: str = "pull") -> ConsumerBatch:
     """Run the reshard on this rank. sources: {producer dp rank: (PackedBatch, first record of that group in it)}
     for every locally held producer group. schema: (stream name -> dtype, channel names), needed only on ranks
-    that hold no producer group. Collective across the ranks of `group` (torch.distributed, NCCL: token data) when
-    distributed; meta_group (gloo, CPU) carries the small size table without a device synchronisation."""
+    that hold no producer group. Collective across the ranks of `group` (torch.distributed NCCL group) when
+    records cross GPUs; meta_group (gloo, CPU) carries the small host tables without a device synchronisation.
+
+    transport "pull" (default): consumers map the producers' buffers (CUDA IPC, dfx_ipc_export/open) and pull the
+    token ranges over NVLink with copy engines; the unpack kernel reads the producers' record metadata straight
+    from peer memory; two device-side NCCL barriers order the pulls against production and reuse.
+    transport "nccl": grouped NCCL send/recv of 16-aligned token ranges + packed metadata (dfx_reshard_pack)."""
     L = _declare()
     rank = plan.rank
     for p in plan.local_src:
@@ -231,13 +244,19 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     stream_specs, ch_names = schema
     t_ = _mark("", None)
     loc = _src_slices(plan, sources)
+    distributed = plan.cross and _distributed(group)
+    pull = distributed and transport == "pull"
 
-    # 1. sizes of every segment (rollouts, tokens), filled by the owner, summed across ranks
+    # 1. per-segment table filled by the owner: rollouts, tokens, first token mod 16 (NCCL alignment),
+    #    and (pull) the absolute token / rollout / record offsets in the owner's arrays
     nseg = len(plan.segs)
-    sizes = np.zeros((nseg, 3), np.int64)  # rollouts, tokens, first token mod 16 (NCCL alignment)
+    sizes = np.zeros((nseg, 6), np.int64)
     for i, (b, r0, r1, s0, s1, t0, t1) in loc.items():
-        sizes[i] = (s1 - s0, t1 - t0, t0 & 15)
-    if plan.cross and _distributed(group):
+        sizes[i] = (s1 - s0, t1 - t0, t0 & 15, t0, s0, r0)
+    peer_addr = {}
+    if pull:
+        sizes, peer_addr = _gather_pull_tables(plan, loc, sizes, group, meta_group, ch_names, stream_specs)
+    elif distributed:
         sizes = all_reduce_host(sizes, group, meta_group, dev)
     t_ = _mark("sizes", t_)
 
@@ -247,14 +266,14 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     rec_off, roll_off, tok_off = [0], [0], [0]
     dst = {}
     for d in groups:
-        s_, t_ = roll_off[-1], tok_off[-1]
+        s_pos, t_pos = roll_off[-1], tok_off[-1]
         for i in seg_of[d]:
-            dst[i] = (rec_off[-1] + int(plan.segs[i][2]), s_, t_)
-            s_ += int(sizes[i, 0])
-            t_ += int(sizes[i, 1])
+            dst[i] = (rec_off[-1] + int(plan.segs[i][2]), s_pos, t_pos)
+            s_pos += int(sizes[i, 0])
+            t_pos += int(sizes[i, 1])
         rec_off.append(rec_off[-1] + int(plan.dest_counts[d]))
-        roll_off.append(s_)
-        tok_off.append(t_)
+        roll_off.append(s_pos)
+        tok_off.append(t_pos)
     order = [i for d in groups for i in seg_of[d]]
 
     # zero-copy: every needed segment is local, from one batch, contiguous and in order
@@ -264,7 +283,13 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
                                                        for k in range(len(order) - 1)):
             r_a, r_b = loc[order[0]][1], loc[order[-1]][2]
             view = b0 if (r_a == 0 and r_b == b0.n_records) else b0.view_records(r_a, r_b)
-            _, sent, recv_b, _ = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)  # peers may need ours
+            if pull:  # peers may pull from us: take part in both barriers
+                _device_barrier(group, dev)
+                _device_barrier(group, dev)
+                sent = sum(int(sizes[i, 1]) for i, (d, p, *_r) in enumerate(plan.segs) if i in loc
+                           for r in plan.dst_ranks[d] if r != rank)
+                return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0)
+            _, sent, recv_b, _ = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)
             return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, recv_b)
 
     # 3. allocate the consumer batch
@@ -290,40 +315,126 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
                 t[dt:dt + (t1 - t0)].copy_(b.streams[k][t0:t1], non_blocking=True)
         metas.append(_meta(b, r0, r1, s0, ch_names, dr, ds, dt))
     t_ = _mark("local copies", t_)
-    # remote segments: one grouped NCCL P2P call (sends of our segments to peers, receives of theirs)
-    recvd, sent, recv_b, staged = _p2p(plan, loc, sizes, dev, st, group, ch_names, (out, dst))
-    t_ = _mark("p2p", t_)
-    # place the received 16-aligned supersets at their exact (unaligned) destination offsets
-    for i, k, buf in staged:
-        head, n_tok = int(sizes[i, 2]), int(sizes[i, 1])
-        dt = dst[i][2]
-        out.streams[k][dt:dt + n_tok].copy_(buf[head:head + n_tok], non_blocking=True)
-    t_ = _mark("place", t_)
-    for i, buf in recvd:
-        n_rec, n_roll = int(plan.segs[i][4]), int(sizes[i, 0])
-        dr, ds, dt = dst[i]
-        base = buf.data_ptr()
-        m = SegMeta()
-        m.ids = base
-        m.cu = base + 8 * n_rec
-        for c in range(len(ch_names)):
-            m.ch[c] = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * c * n_roll
-        m.group_off = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * len(ch_names) * n_roll
-        m.n_rec, m.n_roll, m.dst_rec, m.dst_roll, m.dst_tok = n_rec, n_roll, dr, ds, dt
-        metas.append(m)
+    sent = recv_b = 0
+    recvd = []
+    if pull:
+        _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+        for i in order:
+            if i in loc:
+                continue
+            n_roll, n_tok, _, t0, s0, r0 = (int(x) for x in sizes[i])
+            dr, ds, dt = dst[i]
+            src = plan.src_rank[plan.segs[i][1]]
+            addr = peer_addr[(src, plan.segs[i][1])]
+            for k, t in out.streams.items():
+                esz = t.element_size()
+                _abi.check(L.dfx_copy_async(t.data_ptr() + dt * esz, addr["s:" + k] + t0 * esz, n_tok * esz,
+                                            st.cuda_stream))
+                recv_b += n_tok * esz
+            m = SegMeta()
+            m.ids = addr["ids"] + 8 * r0
+            m.group_off = addr["group_off"] + 4 * r0
+            m.cu = addr["cu"] + 8 * s0
+            for c, name in enumerate(ch_names):
+                m.ch[c] = addr["c:" + name] + 8 * s0
+            m.n_rec, m.n_roll, m.dst_rec, m.dst_roll, m.dst_tok = int(plan.segs[i][4]), n_roll, dr, ds, dt
+            metas.append(m)
+        sent = sum(int(sizes[i, 1]) * sum(torch.empty(0, dtype=dt_).element_size() for dt_ in stream_specs.values())
+                   for i, (d, p, *_r) in enumerate(plan.segs) if i in loc for r in plan.dst_ranks[d] if r != rank)
+    else:
+        # remote segments: one grouped NCCL P2P call (sends of our segments to peers, receives of theirs)
+        recvd, sent, recv_b, staged = _p2p(plan, loc, sizes, dev, st, group, ch_names, (out, dst))
+        # place the received 16-aligned supersets at their exact (unaligned) destination offsets
+        for i, k, buf in staged:
+            head, n_tok = int(sizes[i, 2]), int(sizes[i, 1])
+            dt = dst[i][2]
+            out.streams[k][dt:dt + n_tok].copy_(buf[head:head + n_tok], non_blocking=True)
+        for i, buf in recvd:
+            n_rec, n_roll = int(plan.segs[i][4]), int(sizes[i, 0])
+            dr, ds, dt = dst[i]
+            base = buf.data_ptr()
+            m = SegMeta()
+            m.ids = base
+            m.cu = base + 8 * n_rec
+            for c in range(len(ch_names)):
+                m.ch[c] = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * c * n_roll
+            m.group_off = base + 8 * n_rec + 8 * (n_roll + 1) + 8 * len(ch_names) * n_roll
+            m.n_rec, m.n_roll, m.dst_rec, m.dst_roll, m.dst_tok = n_rec, n_roll, dr, ds, dt
+            metas.append(m)
+    t_ = _mark("transfer", t_)
     if metas:
-        seg_dev = _to_device((SegMeta * len(metas))(*metas), dev)
-        ch_dev = _to_device((C.c_void_p * max(1, len(ch_names)))(*[out.channels[c].data_ptr() for c in ch_names]), dev)
-        _abi.check(L.dfx_reshard_unpack(seg_dev.data_ptr(), len(metas), len(ch_names), out.ids.data_ptr(),
+        segs = (SegMeta * len(metas))(*metas)
+        chp = (C.c_void_p * max(1, len(ch_names)))(*[out.channels[c].data_ptr() for c in ch_names])
+        _abi.check(L.dfx_reshard_unpack(C.cast(segs, C.c_void_p), len(metas), len(ch_names), out.ids.data_ptr(),
                                         out.group_off.data_ptr(), out.roll_group.data_ptr(), out.cu_seqlens.data_ptr(),
-                                        ch_dev.data_ptr(), st.cuda_stream))
-        out._keep = [seg_dev, ch_dev, recvd]
+                                        C.cast(chp, C.c_void_p), st.cuda_stream))
+        out._keep = [recvd]
+    if pull:
+        _device_barrier(group, dev)  # peers may reuse their buffers once every consumer has pulled
     t_ = _mark("unpack", t_)
-    # host metadata of the consumer batch (views and host-side checks need it)
-    out.host_group_off = out.group_off.cpu().numpy()
-    out.host_cu = out.cu_seqlens.cpu().numpy()
-    _mark("host meta", t_)
+    # host offsets of the consumer batch are fetched lazily (PackedBatch.ensure_host_meta): no D2H here
+    out.host_group_off, out.host_cu = None, None
     return ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
+
+
+_BARRIER = {}
+
+
+def _device_barrier(group, dev):
+    """Device-side barrier: a 1-element NCCL all-reduce on the current stream (no host synchronisation). When it
+    completes on this GPU, every rank's stream has executed everything enqueued before its own barrier."""
+    t = _BARRIER.get(dev)
+    if t is None:
+        t = _BARRIER[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
+    torch.distributed.all_reduce(t, group=group)
+
+
+def _export(t: torch.Tensor):
+    h = (C.c_char * 64)()
+    off = C.c_uint64()
+    _abi.check(_declare().dfx_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def _gather_pull_tables(plan: Plan, loc: dict, sizes, group, meta_group, ch_names, stream_specs):
+    """One host all-gather carrying every rank's segment rows and the IPC exports of its producer batches'
+    arrays; returns the global table and {(src rank, producer group): {array: mapped device address}}."""
+    L = _declare()
+    exports = {}
+    roots = {}
+    for i, (b, *_r) in loc.items():
+        p = plan.segs[i][1]
+        key = id(b)
+        if key not in roots:
+            arr = {"ids": b.ids, "group_off": b.group_off, "cu": b.cu_seqlens}
+            for name in ch_names:
+                arr["c:" + name] = b.channels[name]
+            for k in stream_specs:
+                arr["s:" + k] = b.streams[k]
+            roots[key] = {n: _export(t) for n, t in arr.items()}
+        exports[p] = roots[key]
+    mine = ({i: sizes[i].tolist() for i in loc}, exports)
+    world = torch.distributed.get_world_size(group)
+    everyone = [None] * world
+    torch.distributed.all_gather_object(everyone, mine, group=meta_group if meta_group is not None else group)
+    table = np.zeros_like(sizes)
+    addr = {}
+    for r, (rows, exp) in enumerate(everyone):
+        for i, row in rows.items():
+            table[int(i)] = row
+        if r == plan.rank:
+            continue
+        for p, arrs in exp.items():
+            if not any(r2 != r and plan.rank == r2 for d, pp, *_x in plan.segs if pp == p
+                       for r2 in plan.dst_ranks[d]):
+                continue  # this rank never pulls group p
+            out = {}
+            for n, (handle, off) in arrs.items():
+                base = C.c_void_p()
+                _abi.check(L.dfx_ipc_open(handle, 64, C.byref(base)))
+                out[n] = base.value + off
+            addr[(r, int(p))] = out
+    return table, addr
 
 
 def all_reduce_host(a: np.ndarray, group, meta_group, dev) -> np.ndarray:
@@ -411,15 +522,13 @@ def _p2p(plan: Plan, loc: dict, sizes, dev, st, group, ch_names, recv_into):
                         recv_b += buf_k.numel() * buf_k.element_size()
     t_ = _mark("p2p:post-prep", t_)
     if to_pack:
-        seg_dev = _to_device((SegMeta * len(to_pack))(*[m for m, _ in to_pack]), dev)
-        out_dev = _to_device((C.c_void_p * len(to_pack))(*[b.data_ptr() for _, b in to_pack]), dev)
-        _abi.check(L.dfx_reshard_pack(seg_dev.data_ptr(), len(to_pack), len(ch_names), out_dev.data_ptr(),
+        segs = (SegMeta * len(to_pack))(*[m for m, _ in to_pack])
+        outp = (C.c_void_p * len(to_pack))(*[b.data_ptr() for _, b in to_pack])
+        _abi.check(L.dfx_reshard_pack(C.cast(segs, C.c_void_p), len(to_pack), len(ch_names), C.cast(outp, C.c_void_p),
                                       st.cuda_stream))
     t_ = _mark("p2p:pack", t_)
     if ops:
         for w in torch.distributed.batch_isend_irecv(ops):
             w.wait()
     t_ = _mark("p2p:nccl (%d ops)" % len(ops), t_)
-    if to_pack:
-        st.synchronize()  # keep the pack tables alive until the sends completed
     return recvd, sent, recv_b, staged

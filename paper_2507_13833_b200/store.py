@@ -36,8 +36,10 @@ class _Entry:
 
 
 class DeviceBufferStore:
-    def __init__(self, topo: Topology, rank: int, stages: dict, group=None, stream=None, meta_group=None):
+    def __init__(self, topo: Topology, rank: int, stages: dict, group=None, stream=None, meta_group=None,
+                 transport: str = "pull"):
         self.topo, self.rank, self.stages, self.group, self.stream = topo, rank, dict(stages), group, stream
+        self.transport = transport  # "pull" (NVLink peer pulls) or "nccl" (grouped send/recv)
         self.meta_group = meta_group  # CPU (gloo) group for host metadata; data moves over `group` (NCCL)
         self.local_workers = [w for w in range(topo.world) if topo.gpu_of_worker[w] == rank]
         self._entries: dict = {}
@@ -89,7 +91,8 @@ class DeviceBufferStore:
         counts = self._agree_counts(counts, local)
         plan = Plan(self.topo, sp.produced, to, counts, self.rank)
         sources = {p: (e.by_group[p], 0) for p in local}
-        e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group)
+        e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
+                           transport=self.transport)
         e.consumed = to
         e.by_group = {}
         self.bytes_sent += e.ready.bytes_sent

@@ -32,12 +32,12 @@ full = dfx.PackedBatch.from_host(sb.ids, sb.group_off, sb.cu_seqlens, {"reward":
                                  {k: getattr(sb, k)[:T] for k in ("token_id", "lp", "old_lp", "ref_lp", "mask")},
                                  device=dev)
 dfx.fn_group_advantage(dfx.NodeSpec("adv"), full, dfx.StageContext())
-for name in ("dense", "cross"):
+for name, transport in (("dense", "pull"), ("cross", "pull"), ("dense", "nccl"), ("cross", "nccl")):
     B, W, dp_p, tp_p, dp_c, tp_c = (int(x) for x in g[f"{name}_cfg"])
     topo = Topology.store_per_gpu(world, W) if B == world else Topology(B, W, tuple(w * world // (B * W)
                                                                                    for w in range(B * W)))
     store = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(Layout(dp_p, tp_p), Layout(dp_c, tp_c))},
-                              meta_group=meta)
+                              meta_group=meta, transport=transport)
     per = 16 // dp_p
     for p in range(dp_p):
         for t in range(tp_p):
@@ -52,7 +52,7 @@ for name in ("dense", "cross"):
         assert blob.tobytes() == g[f"{name}_blob_{d}"].tobytes(), (name, rank, d)
         assert got.n_records == int(g[f"{name}_counts"][d])
     assert store.bytes_sent > 0 or not cb.groups, name
-    print(f"rank {rank} {name}: dests {cb.groups} sent {store.bytes_sent} recv {store.bytes_recv} zero_copy "
+    print(f"rank {rank} {name}/{transport}: dests {cb.groups} sent {store.bytes_sent} recv {store.bytes_recv} zero_copy "
           f"{cb.zero_copy}", flush=True)
 dist.barrier()
 print("RESHARD_OK", flush=True)

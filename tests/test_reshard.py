@@ -200,6 +200,7 @@ def test_device_reshard_materialized_copy(O, dfx):
     _, idx = O.reshard_placement(2, 2, 4, 1, 2, 2, [8] * 4)
     assert (cb.batch.ids.cpu().numpy().view(np.uint64) == sb.ids[idx]).all()
     # token streams of each destination record equal the source record's
+    cb.batch.ensure_host_meta()
     go, cu = cb.batch.host_group_off, cb.batch.host_cu
     lp = cb.batch.streams["lp"].cpu().numpy()
     for k, r in enumerate(idx.tolist()):

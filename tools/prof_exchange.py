@@ -21,6 +21,7 @@ from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan  # noq
 ap = argparse.ArgumentParser()
 ap.add_argument("--records", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--transport", default="pull")
 a = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
@@ -34,7 +35,7 @@ dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
 wpg = max(2, 8 // world)
 topo = R.Topology.store_per_gpu(world, wpg)
 prod, cons = R.Layout(world * wpg, 1), R.Layout(world * wpg // 2, 2)
-st = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(prod, cons)}, meta_group=meta)
+st = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(prod, cons)}, meta_group=meta, transport=a.transport)
 local_p = [p for p in range(prod.dp) if topo.gpu_of_worker[p] == rank]
 per = a.records // len(local_p)
 
@@ -69,6 +70,6 @@ for it in range(a.iters + 1):
     T["total ensure_ready"] = T.get("total ensure_ready", 0) + time.perf_counter() - t0
     for _ in st.local_workers:
         st.worker_done(it)
-print(f"rank {rank}: " + ", ".join(f"{k} {1e3 * v / a.iters:.3f} ms" for k, v in T.items()) +
+print(f"rank {rank} [{a.transport}]: " + ", ".join(f"{k} {1e3 * v / a.iters:.3f} ms" for k, v in T.items()) +
       f" | sent {cb.bytes_sent / 1e6:.1f} MB zero_copy {cb.zero_copy}", flush=True)
 dist.destroy_process_group()
