@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--records", type=int, default=C2["records"])
+    ap.add_argument("--workers", type=int, default=8,
+                    help="box placement: logical workers (the reference's W); N=8 GPUs with 8 workers puts TP "
+                         "partners on different GPUs -- --workers 4 on 4 GPUs previews that path")
     ap.add_argument("--placement", default="box", choices=["box", "store"],
                     help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
                          "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")
@@ -143,12 +146,12 @@ class DagSlice:
 
     STAGE = "group_advantage_compute"
 
-    def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box"):
+    def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box", workers=8):
         self.dfx, self.ctx, self.it = dfx, ctx, 0
         self.placement = placement
         if placement == "box":
-            self.topo = Topology.box(8, world)
-            self.prod, self.cons = Layout(8, 1), Layout(4, 2)
+            self.topo = Topology.box(workers, world)
+            self.prod, self.cons = Layout(workers, 1), Layout(workers // 2, 2)
         else:
             wpg = max(2, 8 // world)
             self.topo = Topology.store_per_gpu(world, wpg)
@@ -221,7 +224,8 @@ def run_dfx(args):
     ctx = dfx.StageContext()
     ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
     stream = torch.cuda.current_stream(dev)
-    resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement)
+    resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement,
+                    args.workers)
 
     ev0, ev1 = C.c_void_p(), C.c_void_p()
     _abi.check(L.dfx_event_create(C.byref(ev0)))

@@ -397,12 +397,18 @@ def _export(t: torch.Tensor):
 
 
 def _gather_pull_tables(plan: Plan, loc: dict, sizes, group, meta_group, ch_names, stream_specs):
-    """One host all-gather carrying every rank's segment rows and the IPC exports of its producer batches'
-    arrays; returns the global table and {(src rank, producer group): {array: mapped device address}}."""
+    """One fixed-size int64 all-gather (CPU group) carrying every rank's segment rows and the IPC exports
+    (64-byte handle + offset) of its producer batches' arrays; returns the global table and
+    {(src rank, producer group): {array: mapped device address}}."""
     L = _declare()
-    exports = {}
+    names = ["ids", "group_off", "cu"] + ["c:" + c for c in ch_names] + ["s:" + k for k in stream_specs]
+    nseg, dp_p, na = len(plan.segs), plan.produced.dp, len(names)
+    width = nseg * 6 + dp_p * na * 9
+    mine = np.zeros(width, np.int64)
+    exp = mine[nseg * 6:].reshape(dp_p, na, 9)
     roots = {}
     for i, (b, *_r) in loc.items():
+        mine[i * 6:(i + 1) * 6] = sizes[i]
         p = plan.segs[i][1]
         key = id(b)
         if key not in roots:
@@ -411,29 +417,36 @@ def _gather_pull_tables(plan: Plan, loc: dict, sizes, group, meta_group, ch_name
                 arr["c:" + name] = b.channels[name]
             for k in stream_specs:
                 arr["s:" + k] = b.streams[k]
-            roots[key] = {n: _export(t) for n, t in arr.items()}
-        exports[p] = roots[key]
-    mine = ({i: sizes[i].tolist() for i in loc}, exports)
+            rows = np.zeros((na, 9), np.int64)
+            for j, n in enumerate(names):
+                h, off = _export(arr[n])
+                rows[j, :8] = np.frombuffer(h, np.int64)
+                rows[j, 8] = off
+            roots[key] = rows
+        exp[p] = roots[key]
     world = torch.distributed.get_world_size(group)
-    everyone = [None] * world
-    torch.distributed.all_gather_object(everyone, mine, group=meta_group if meta_group is not None else group)
+    cpu = meta_group is not None
+    t = torch.from_numpy(mine)
+    if not cpu:
+        t = t.cuda()
+    gathered = [torch.empty_like(t) for _ in range(world)]
+    torch.distributed.all_gather(gathered, t, group=meta_group if cpu else group)
+    allrows = np.stack([g.cpu().numpy() for g in gathered])
     table = np.zeros_like(sizes)
+    for i, (d, p, *_x) in enumerate(plan.segs):
+        table[i] = allrows[plan.src_rank[p], i * 6:(i + 1) * 6]
     addr = {}
-    for r, (rows, exp) in enumerate(everyone):
-        for i, row in rows.items():
-            table[int(i)] = row
-        if r == plan.rank:
+    for i, (d, p, *_x) in enumerate(plan.segs):
+        src = plan.src_rank[p]
+        if src == plan.rank or plan.rank not in plan.dst_ranks[d] or (src, int(p)) in addr:
             continue
-        for p, arrs in exp.items():
-            if not any(r2 != r and plan.rank == r2 for d, pp, *_x in plan.segs if pp == p
-                       for r2 in plan.dst_ranks[d]):
-                continue  # this rank never pulls group p
-            out = {}
-            for n, (handle, off) in arrs.items():
-                base = C.c_void_p()
-                _abi.check(L.dfx_ipc_open(handle, 64, C.byref(base)))
-                out[n] = base.value + off
-            addr[(r, int(p))] = out
+        rows = allrows[src, nseg * 6:].reshape(dp_p, na, 9)[p]
+        out = {}
+        for j, n in enumerate(names):
+            base = C.c_void_p()
+            _abi.check(L.dfx_ipc_open(rows[j, :8].tobytes(), 64, C.byref(base)))
+            out[n] = base.value + int(rows[j, 8])
+        addr[(src, int(p))] = out
     return table, addr
 
 

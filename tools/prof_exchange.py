@@ -5,6 +5,8 @@ Prints per-rank wall time of put / ensure_ready (split into plan, sizes, alloc+l
 metadata) for the bench's C2 batch.
 """
 import argparse
+
+import numpy as np
 import os
 import sys
 import time
@@ -22,6 +24,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--records", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--transport", default="pull")
+ap.add_argument("--placement", default="store")
+ap.add_argument("--workers", type=int, default=8)
 a = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
@@ -32,9 +36,13 @@ b = dfx.PackedBatch.synthetic(1, a.records, 16, dfx.TokenDist("uniform", 0, 1, 4
                               first_id=rank * a.records)
 ctx = dfx.StageContext()
 dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
-wpg = max(2, 8 // world)
-topo = R.Topology.store_per_gpu(world, wpg)
-prod, cons = R.Layout(world * wpg, 1), R.Layout(world * wpg // 2, 2)
+if a.placement == "box":
+    topo = R.Topology.box(a.workers, world)
+    prod, cons = R.Layout(a.workers, 1), R.Layout(a.workers // 2, 2)
+else:
+    wpg = max(2, 8 // world)
+    topo = R.Topology.store_per_gpu(world, wpg)
+    prod, cons = R.Layout(world * wpg, 1), R.Layout(world * wpg // 2, 2)
 st = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(prod, cons)}, meta_group=meta, transport=a.transport)
 local_p = [p for p in range(prod.dp) if topo.gpu_of_worker[p] == rank]
 per = a.records // len(local_p)
@@ -57,7 +65,9 @@ def timed(name, fn):
 
 R.Plan.__init__ = timed("plan", R.Plan.__init__)
 R.PROFILE = T
+allocs = []
 for it in range(a.iters + 1):
+    allocs.append(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))
     if it == 1:
         T.clear()
     torch.cuda.synchronize()
@@ -71,5 +81,6 @@ for it in range(a.iters + 1):
     for _ in st.local_workers:
         st.worker_done(it)
 print(f"rank {rank} [{a.transport}]: " + ", ".join(f"{k} {1e3 * v / a.iters:.3f} ms" for k, v in T.items()) +
-      f" | sent {cb.bytes_sent / 1e6:.1f} MB zero_copy {cb.zero_copy}", flush=True)
+      f" | sent {cb.bytes_sent / 1e6:.1f} MB zero_copy {cb.zero_copy} | cudaMalloc per iter {list(np.diff(allocs))}",
+      flush=True)
 dist.destroy_process_group()
