@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 METRIC = "post-rollout tokens/s (adv+loss+reshard) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "tokens/s"
 C2 = dict(records=1024, n_roll=16, dist=("uniform", 0, 1, 4096), seed=1)
+C5 = dict(records=4096, n_roll=16, dist=("skewed", 0, 1, 16384), seed=11)
 BYTES_PER_TOKEN = 17      # lp, old_lp, ref_lp (3x4) + mask (1) + advantage write (4)
 BYTES_PER_ROLLOUT = 16    # f64 advantage read + i64 cu_seqlens read
 
@@ -49,7 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--records", type=int, default=C2["records"])
+    ap.add_argument("--records", type=int, default=None, help="prompts per GPU (default: the workload's)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: 1024 prompts x 16 x U[1,4096] per GPU (weak scaling, the headline); c5: BASELINE "
+                         "config 5, 4096 prompts x 16 x skewed <=16k tokens split over the GPUs (strong scaling)")
     ap.add_argument("--workers", type=int, default=8,
                     help="box placement: logical workers (the reference's W); N=8 GPUs with 8 workers puts TP "
                          "partners on different GPUs -- --workers 4 on 4 GPUs previews that path")
@@ -216,9 +220,16 @@ def run_dfx(args):
     from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan
 
     L = _abi.lib()
-    R, n = args.records, C2["n_roll"]
-    distrib = dfx.TokenDist(*C2["dist"])
-    batch = dfx.PackedBatch.synthetic(C2["seed"], R, n, distrib, device=dev, first_id=rank * R)
+    n = C2["n_roll"]
+    if args.workload == "c5":
+        R = args.records or C5["records"] // world
+        distrib, seed = dfx.TokenDist(*C5["dist"]), C5["seed"]
+        wl = f"C5: {R * world} prompts x n={n} x skewed[1,16384] tokens over {world} GPU"
+    else:
+        R = args.records or C2["records"]
+        distrib, seed = dfx.TokenDist(*C2["dist"]), C2["seed"]
+        wl = f"C2 per GPU: {R} prompts x n={n} x UNIFORM[1,4096] tokens"
+    batch = dfx.PackedBatch.synthetic(seed, R, n, distrib, device=dev, first_id=rank * R)
     torch.cuda.synchronize()
     tokens_local = batch.token_span
     ctx = dfx.StageContext()
@@ -311,13 +322,12 @@ def run_dfx(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 group stats/accumulators)",
+            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32 (f64 group stats/accumulators)",
             "data": "synthetic (keyed SplitMix64, generated on device; SURVEY.md §8(d))",
-            "config": {"workload": f"C2 per GPU: {R} prompts x n={n} x UNIFORM[1,4096] tokens "
-                                   f"(~{tokens_local/1e6:.1f}M tokens/GPU), GRPO adv -> DataBuffer reshard "
+            "config": {"workload": f"{wl} (~{tokens_local/1e6:.1f}M tokens/GPU), GRPO adv -> DataBuffer reshard "
                                    f"(dp_p -> dp_p/2, tp 2) -> clipped loss + k3 KL token-mean",
                        "tokens_per_gpu": tokens_local, "global_tokens": int(tokens_total),
-                       "reshard": resh.describe(), "l2": "inputs (571 MB/GPU) larger than the 126 MB L2; no flush",
+                       "reshard": resh.describe(), "l2": f"inputs ({bytes_launch / 1e6:.0f} MB/GPU) larger than the 126 MB L2; no flush",
                        "parallelism": f"dp{world} (logical dp8->dp4 over {world} GPU)",
                        "cuda_graph": graph is not None},
             "e2e": e2e, "gpu_launches": resh.launches_per_step(), "roofline": roof, "cpu_baseline": cpu,
