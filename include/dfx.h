@@ -110,11 +110,15 @@ dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream s
  *   delta_t = r_t + gamma*m1*v1 - V_t ;  A_t = delta_t + gamma*lam*m1*A_{t+1} ;  R_t = A_t + V_t
  * computed in f64 inside the kernel, stored f32. Optionally writes the masked
  * whitening sums whiten[3] = {sum m*A, sum m*A^2, sum m} (device f64). */
-/* Parallel over the whole token line: 256-token slots claimed by persistent
- * warps in reverse order, carries resolved by a decoupled look-back across the
- * slots of a rollout. Workspace (dfx_gae_workspace_bytes) must be zero-filled
- * once at allocation; the kernel keeps it consistent across calls (epoch-tagged
- * flags, self-resetting tickets), so it can be reused and graph-captured. */
+/* One reverse affine scan over the whole token line (the chain breaks at rollout
+ * ends by itself): a prep kernel marks rollout ends in a token bitmap, a
+ * single-pass decoupled look-back scan over 2048-token CTA tiles does the rest
+ * (f32 inside a thread's chunk, f64 across chunks), and with whitening a
+ * finish kernel reduces the per-tile sums in tile order (deterministic).
+ * Workspace (dfx_gae_workspace_bytes) must be zero-filled once at allocation;
+ * the kernels keep it consistent across calls (epoch-tagged tile records, the
+ * end bitmap cleared as it is consumed), so it can be reused and
+ * graph-captured. */
 size_t dfx_gae_workspace_bytes(int64_t n_rollouts, int64_t token_span);
 dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
                    float* adv, float* ret, double* whiten, void* workspace, size_t ws_bytes, dfx_stream stream);

@@ -97,6 +97,10 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
                ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// bulk prefetch of [p, p+bytes) into L2 (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // order earlier generic-proxy shared-memory accesses before later async-proxy (TMA) writes
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
