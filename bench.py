@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--workers", type=int, default=8,
                     help="box placement: logical workers (the reference's W); N=8 GPUs with 8 workers puts TP "
                          "partners on different GPUs -- --workers 4 on 4 GPUs previews that path")
+    ap.add_argument("--materialize", action="store_true",
+                    help="copy remote records into a local consumer batch before the loss (default: the loss kernel "
+                         "reads them in place over NVLink)")
     ap.add_argument("--placement", default="box", choices=["box", "store"],
                     help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
                          "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")
@@ -150,8 +153,10 @@ class DagSlice:
 
     STAGE = "group_advantage_compute"
 
-    def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box", workers=8):
+    def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box", workers=8,
+                 lazy=True, dev=None):
         self.dfx, self.ctx, self.it = dfx, ctx, 0
+        self.lazy, self.dev = lazy, dev
         self.placement = placement
         if placement == "box":
             self.topo = Topology.box(workers, world)
@@ -177,9 +182,14 @@ class DagSlice:
         dfx.fn_group_advantage(dfx.NodeSpec(self.STAGE), batch, ctx)
         for j, p in enumerate(self.local_p):
             self.store.put(self.STAGE, self.it, p, 0, batch.view_records(j * self.per, (j + 1) * self.per))
-        cb = self.store.ensure_ready(self.STAGE, self.it, self.cons)
-        res = dfx.ppo_loss(cb.batch, ctx, adv_source="rollout", loss_group_off=cb.roll_off, adv_tok_out=True,
-                           events=events)
+        cb = self.store.ensure_ready(self.STAGE, self.it, self.cons, lazy=self.lazy)
+        if cb.sources is not None:  # TP partner's records read in place over NVLink by the loss kernel
+            srcs = [x for grp in cb.sources for x in grp]
+            res = dfx.ppo_loss_sources(srcs, ctx, loss_group_off=cb.roll_off, adv_tok_out=True, events=events,
+                                       device=self.dev)
+        else:
+            res = dfx.ppo_loss(cb.batch, ctx, adv_source="rollout", loss_group_off=cb.roll_off, adv_tok_out=True,
+                               events=events)
         for _ in self.store.local_workers:
             self.store.worker_done(self.it)
         self.it += 1
@@ -187,12 +197,18 @@ class DagSlice:
         return res, cb.batch
 
     def launches_per_step(self):
-        # grpo_adv + loss_slots + finalize (+ pack, unpack and NCCL P2P when records cross GPUs)
-        return 3 + (3 if self.cross else 0)
+        # grpo_adv + loss_slots + finalize; records crossing GPUs: + the materializing unpack kernel (lazy: none,
+        # the loss kernel reads the partner's records over NVLink)
+        return 3 + (1 if self.cross and not self.lazy else 0)
 
     def describe(self):
-        mode = ("zero-copy views: every consumer group's TP workers and producer groups share a GPU"
-                if not self.cross else "records cross GPUs over NVLink (grouped NCCL P2P) + pack/unpack kernels")
+        if not self.cross:
+            mode = "zero-copy views: every consumer group's TP workers and producer groups share a GPU"
+        elif self.lazy:
+            mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC) and the "
+                    "loss kernel streams it over NVLink in place (dfx_ppo_loss_multi), no copy")
+        else:
+            mode = "records cross GPUs: copy-engine pulls over NVLink into a consumer batch + unpack kernel"
         t = self.topo
         return (f"{self.placement} placement B={t.num_nodes} W={t.workers_per_node}: dp{self.prod.dp}(tp1) -> "
                 f"dp{self.cons.dp}(tp2) over {self.world} GPU; {mode}")
@@ -236,7 +252,7 @@ def run_dfx(args):
     ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
     stream = torch.cuda.current_stream(dev)
     resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement,
-                    args.workers)
+                    args.workers, lazy=not args.materialize, dev=dev)
 
     ev0, ev1 = C.c_void_p(), C.c_void_p()
     _abi.check(L.dfx_event_create(C.byref(ev0)))

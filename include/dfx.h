@@ -174,6 +174,26 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
                         const dfx_loss_args* args, void* workspace, size_t ws_bytes,
                         dfx_stream stream);
 
+/* Multi-source loss (the reshard's consumer side fused with the loss): one call
+ * over up to 4 packed batches, each in its own token coordinates -- e.g. the
+ * local producer group and the TP partner's producer group mapped from the
+ * partner GPU (dfx_ipc_open), read over NVLink by the streaming kernel itself
+ * instead of being copied first. Rollouts are numbered across the sources in
+ * order; loss_group_off (args) uses that numbering. Per-token inputs/outputs
+ * are per source: args->adv_roll/adv_tok_in/adv_tok_out/dlogp are ignored.
+ * DFX_ADV_GROUP_FUSED needs a single source. */
+typedef struct dfx_loss_src {
+  dfx_packed b;              /* cu_seqlens, lp, old_lp, ref_lp, mask (device or peer-mapped pointers) */
+  int64_t token_base, token_span;
+  const double* adv_roll;    /* DFX_ADV_ROLLOUT: this source's per-rollout advantages */
+  const float* adv_tok_in;   /* DFX_ADV_TOKEN */
+  float* adv_tok_out;        /* nullable; indexed like this source's token streams */
+  float* dlogp;              /* nullable (all sources or none); likewise */
+} dfx_loss_src;
+size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_src, int32_t n_loss_groups);
+dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
+                              const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream);
+
 /* Device-side error flags written by kernels (e.g. an empty record seen by the
  * fused GRPO path). Reads flags (device int32) and returns the status. Syncs. */
 dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream);

@@ -39,6 +39,12 @@ class LossArgs(C.Structure):
                 ("ev_main_end", P)]
 
 
+class LossSrc(C.Structure):
+    """dfx_loss_src (include/dfx.h): one token source of dfx_ppo_loss_multi."""
+    _fields_ = [("b", Packed), ("token_base", i64), ("token_span", i64), ("adv_roll", P), ("adv_tok_in", P),
+                ("adv_tok_out", P), ("dlogp", P)]
+
+
 LOSS_OUT_FIELDS = ("loss", "pg_loss", "kl", "clipfrac", "approx_kl", "n_tokens", "n_seqs")
 
 _lib = None
@@ -68,6 +74,9 @@ def _declare(L):
     L.dfx_ppo_loss_workspace_bytes.restype = sz
     L.dfx_ppo_loss_workspace_bytes.argtypes = [i64, i64, i32]
     L.dfx_ppo_loss.argtypes = [C.POINTER(Packed), i64, i64, C.POINTER(LossCfg), C.POINTER(LossArgs), P, sz, P]
+    L.dfx_ppo_loss_multi_workspace_bytes.restype = sz
+    L.dfx_ppo_loss_multi_workspace_bytes.argtypes = [C.POINTER(LossSrc), i32, i32]
+    L.dfx_ppo_loss_multi.argtypes = [C.POINTER(LossSrc), i32, C.POINTER(LossCfg), C.POINTER(LossArgs), P, sz, P]
     L.dfx_check_flags.argtypes = [P, P]
     L.dfx_synth_tokens.argtypes = [u64, P, i64, i32, P, i64, i64, P, P, P, P, P, P, P, P]
     L.dfx_event_create.argtypes = [C.POINTER(P)]
@@ -77,6 +86,7 @@ def _declare(L):
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     for name in ("dfx_grpo_advantage", "dfx_broadcast_advantage", "dfx_ppo_advantage", "dfx_gae", "dfx_ppo_loss",
+                 "dfx_ppo_loss_multi",
                  "dfx_check_flags", "dfx_synth_tokens", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
                  "dfx_event_elapsed_ms"):
         getattr(L, name).restype = i32
@@ -84,7 +94,8 @@ def _declare(L):
 
 # every symbol include/dfx.h declares (checked by tests/test_abi.py against the header and the .so)
 EXPORTS = ("dfx_last_error", "dfx_version", "dfx_grpo_advantage", "dfx_broadcast_advantage", "dfx_ppo_advantage",
-           "dfx_gae_workspace_bytes", "dfx_gae", "dfx_ppo_loss_workspace_bytes", "dfx_ppo_loss", "dfx_check_flags",
+           "dfx_gae_workspace_bytes", "dfx_gae", "dfx_ppo_loss_workspace_bytes", "dfx_ppo_loss",
+           "dfx_ppo_loss_multi_workspace_bytes", "dfx_ppo_loss_multi", "dfx_check_flags",
            "dfx_synth_tokens", "dfx_event_create", "dfx_event_destroy", "dfx_event_record", "dfx_event_elapsed_ms")
 
 

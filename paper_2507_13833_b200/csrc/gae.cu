@@ -74,6 +74,9 @@ __device__ __forceinline__ double rec_c(const ulonglong2& r) { return (double)__
 // ---- prep: rollout-end bitmap + epoch ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gae_prep_kernel(const int64_t* __restrict__ cu, int64_t n_seq, int64_t base,
                                                        uint32_t* __restrict__ ends, unsigned long long* ticket) {
+  // the scan kernel is launched as a programmatic dependent: let it start its loads now; it waits for this
+  // grid's completion (griddepcontrol.wait) before reading the bitmap or the epoch
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s == 0) ticket[2] = (ticket[2] + 1ull) & 0x3fffffffull;
   if (s >= n_seq) return;
@@ -313,6 +316,227 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_tile_kernel(GaeParams p) {
 
 
 
+
+// ---------------------------------------------------------------------------------------------------------------
+// Shared-memory tiles (default): a tile of THREADS*32 tokens is bulk-loaded (TMA) into shared memory and each
+// thread owns 32 consecutive tokens = 8 chunks of 4. A tile is 4-8x longer than a register tile, so the fixed
+// cost of its look-back (L2 round trips) is spread over more tokens, while registers stay low because values are
+// re-read from shared memory. Chunks are visited in a per-lane rotated order (chunk (j + lane) & 7), which makes
+// the 128-bit shared accesses of a warp conflict-free; the in-order dependency is restored by composing the
+// eight chunk maps in order afterwards (pass 1) and by deriving every chunk's carry-in before pass 2. Interior
+// tiles write A and R back over r and V in shared memory and store them with two bulk copies; the (at most two)
+// boundary tiles store per token.
+// ---------------------------------------------------------------------------------------------------------------
+template <int THREADS>
+struct SmemTile {
+  static constexpr int TILE = THREADS * 32;
+  static constexpr uint32_t kR = 0, kV = TILE * 4 + 16, kM = 2 * (TILE * 4 + 16), kBytes = kM + TILE + 16;
+};
+
+template <int THREADS, int MINB, bool WHITEN>
+__global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
+  using L = SmemTile<THREADS>;
+  constexpr int TILE = L::TILE, NW = THREADS / 32;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* s_r = reinterpret_cast<float*>(sm + L::kR);
+  float* s_v = reinterpret_cast<float*>(sm + L::kV);
+  uint8_t* s_m = sm + L::kM;
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ Aff s_warp[NW];
+  __shared__ double s_X;
+  __shared__ double s_red[NW][3];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t tile = p.n_tiles - 1 - (int64_t)blockIdx.x;
+  const int64_t T0 = p.base + tile * TILE;
+  const int64_t rd_end = (p.end + 15) & ~int64_t(15);
+  const uint32_t n = (uint32_t)min((int64_t)TILE, rd_end - T0);  // tokens resident in shared memory (16-multiple)
+  const bool interior = T0 >= p.begin && T0 + TILE <= p.end;
+  const int64_t c0 = T0 + (int64_t)tid * 32;
+
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+    mbar_arrive_expect_tx(&s_bar, 9u * n);
+    tma_load_1d(s_r, p.rew + T0, 4u * n, &s_bar);
+    tma_load_1d(s_v, p.val + T0, 4u * n, &s_bar);
+    tma_load_1d(s_m, p.mask + T0, n, &s_bar);
+    // the token after the tile (V, mask) sits one past the tile in shared memory
+    const int64_t tn = T0 + TILE;
+    s_v[TILE] = tn < p.end ? __ldg(p.val + tn) : 0.0f;
+    s_m[TILE] = tn < p.end ? __ldg(p.mask + tn) : (uint8_t)0;
+    if (p.pf_dist > 0 && tile >= p.pf_dist) {  // keep HBM busy: the next wave's tile into L2
+      const int64_t T0p = p.base + (tile - p.pf_dist) * TILE;
+      const uint32_t np = (uint32_t)min((int64_t)TILE, rd_end - T0p);
+      l2_prefetch(p.rew + T0p, 4u * np);
+      l2_prefetch(p.val + T0p, 4u * np);
+      l2_prefetch(p.mask + T0p, np);
+    }
+  }
+  // (programmatic dependent launch: everything above overlapped the prep kernel; the bitmap and epoch need it done)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // this thread's rollout-end bits (32 tokens = one aligned 32-bit word of the bitmap), cleared once read
+  uint32_t last = 0u;
+  if (c0 < rd_end) {
+    uint32_t* ew = reinterpret_cast<uint32_t*>(p.ends) + ((c0 - p.base) >> 5);
+    last = __ldcg(ew);
+    if (last) *ew = 0u;
+  }
+  uint32_t ident = 0u;
+  if (!(c0 >= p.begin && c0 + 32 <= p.end)) {
+    for (int q = 0; q < 32; ++q)
+      if (c0 + q < p.begin || c0 + q >= p.end) ident |= 1u << q;
+  }
+  unsigned int epoch;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(epoch) : "l"(p.ticket + 2) : "memory");
+  const unsigned int F_AGG = (epoch << 2) | 1u, F_INC = (epoch << 2) | 2u;
+  const float gam = (float)p.gamma, glf = (float)p.gl;
+  __syncthreads();  // s_bar initialised, next-token slot written
+  mbar_wait(&s_bar, 0);
+
+  // pass 1: chunk maps in a per-lane rotated order starting at chunk s = lane & 7 (conflict-free 128-bit shared
+  // reads), folded into tail = C_s o ... o C_7 and head = C_0 o ... o C_(s-1); the thread map is head o tail.
+  // link bit q: token q's successor is in the same rollout and unmasked. Tokens outside the batch are identities
+  // (ident) and never stored.
+  const int s0 = lane & 7;
+  const float vn_cross = s_v[tid * 32 + 32];  // first V of the next thread (or the token after the tile)
+  float Hd = 0.0f, Hc = 1.0f, Td = 0.0f, Tc = 1.0f;
+  uint32_t link = 0u, mbits = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int ch = (s0 + j) & 7;
+    const int i0 = tid * 32 + ch * 4;
+    const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
+    const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
+    const uint32_t m4 = *reinterpret_cast<const uint32_t*>(s_m + i0);
+    const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
+    const uint32_t mnx = s_m[i0 + 4] ? 1u : 0u;
+    const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    float fd = 0.0f, fc = 1.0f;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      const int q = ch * 4 + k;
+      const uint32_t mnext = k == 3 ? mnx : (((m4 >> (8 * (k + 1))) & 0xffu) ? 1u : 0u);
+      const bool lk = mnext && !((last >> q) & 1u);
+      const float vnext = k == 3 ? vnx : vv[k + 1];
+      const float dq = (lk ? fmaf(gam, vnext, rr[k]) : rr[k]) - vv[k];
+      if (!((ident >> q) & 1u)) {
+        fd = lk ? fmaf(glf, fd, dq) : dq;
+        fc = lk ? fc * glf : 0.0f;
+      }
+      link |= (lk ? 1u : 0u) << q;
+      mbits |= (((m4 >> (8 * k)) & 0xffu) ? 1u : 0u) << q;
+    }
+    if (ch >= s0) {  // append on the right: F o C
+      Td = fmaf(Tc, fd, Td);
+      Tc *= fc;
+    } else {
+      Hd = fmaf(Hc, fd, Hd);
+      Hc *= fc;
+    }
+  }
+  Aff S{(double)fmaf(Hc, Td, Hd), (double)(Hc * Tc)};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double od = __shfl_down_sync(kFull, S.d, o), oc = __shfl_down_sync(kFull, S.c, o);
+    if (lane + o < 32) S = compose(S, Aff{od, oc});
+  }
+  if (lane == 0) s_warp[wid] = S;
+  Aff E{__shfl_down_sync(kFull, S.d, 1), __shfl_down_sync(kFull, S.c, 1)};
+  if (lane == 31) E = Aff{0.0, 1.0};
+  __syncthreads();
+  if (wid == 0) {
+    Aff tot{0.0, 1.0};
+#pragma unroll
+    for (int w = NW - 1; w >= 0; --w) tot = compose(s_warp[w], tot);
+    if (lane == 0) rec_store(p.rec + tile, tot.d, (float)tot.c, tot.c == 0.0 ? F_INC : F_AGG);
+    const double X = gae_lookback(p, tile, F_AGG, F_INC, lane);
+    if (lane == 0) {
+      if (tot.c != 0.0) rec_store(p.rec + tile, fma(tot.c, X, tot.d), 0.0f, F_INC);
+      s_X = X;
+    }
+  }
+  __syncthreads();
+  double Xd = s_X;
+#pragma unroll
+  for (int w = NW - 1; w >= 0; --w)
+    if (w > wid) Xd = fma(s_warp[w].c, Xd, s_warp[w].d);
+  // pass 2 in descending cyclic order from chunk s-1: chunks s-1 .. 0 start from the carry tail(X_in), chunks
+  // 7 .. s from X_in. Interior tiles write A over r at once and R over V one chunk late, after the chunk below
+  // has read this chunk's first V as its successor value.
+  const float Xin = (float)fma(E.c, Xd, E.d);
+  float X = fmaf(Tc, Xin, Td);
+  float wa = 0.0f, wa2 = 0.0f;
+  float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
+  int pend_i = -1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int ch = (s0 - 1 - j) & 7;
+    if (j == s0) X = Xin;
+    const int i0 = tid * 32 + ch * 4;
+    const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
+    const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
+    const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
+    if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+    const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    float oa[4], orr[4];
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      const int q = ch * 4 + k;
+      const bool lk = (link >> q) & 1u;
+      const float vnext = k == 3 ? vnx : vv[k + 1];
+      const float dq = (lk ? fmaf(gam, vnext, rr[k]) : rr[k]) - vv[k];
+      const float A = lk ? fmaf(glf, X, dq) : dq;
+      X = ((ident >> q) & 1u) ? X : A;
+      oa[k] = X;
+      orr[k] = X + vv[k];
+      if (WHITEN) {
+        const float mw = ((mbits & ~ident) >> q) & 1u ? 1.0f : 0.0f;
+        wa = fmaf(mw, X, wa);
+        wa2 = fmaf(mw * X, X, wa2);
+      }
+    }
+    if (interior) {
+      *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
+      pendR = make_float4(orr[0], orr[1], orr[2], orr[3]);
+      pend_i = i0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((ident >> (ch * 4 + k)) & 1u)) {
+          p.adv[c0 + ch * 4 + k] = oa[k];
+          p.ret[c0 + ch * 4 + k] = orr[k];
+        }
+      }
+    }
+  }
+  if (interior) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+  if (interior) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_1d(p.adv + T0, s_r, 4u * TILE);
+      tma_store_1d(p.ret + T0, s_v, 4u * TILE);
+      tma_store_commit_and_wait();
+    }
+  }
+  if (WHITEN) {
+    const double wad = warp_sum((double)wa), wa2d = warp_sum((double)wa2);
+    const double wm = warp_sum((double)__popc(mbits & ~ident));
+    if (lane == 0) {
+      s_red[wid][0] = wad;
+      s_red[wid][1] = wa2d;
+      s_red[wid][2] = wm;
+    }
+    __syncthreads();
+    if (tid < 3) {
+      double t3 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t3 += s_red[w][tid];
+      p.part[(int64_t)tid * p.n_tiles + tile] = t3;
+    }
+  }
+}
+
 // ---- whitening sums: fixed-shape reduction of the per-tile partials ---------------------------------------------
 __global__ void __launch_bounds__(256) gae_finish_kernel(const double* __restrict__ part, int64_t n_tiles,
                                                          double* __restrict__ whiten) {
@@ -358,15 +582,49 @@ GaeWs gae_ws_layout(int64_t token_span) {
   return w;
 }
 
-// Tuning knob (benchmarking only): DFX_GAE_VARIANT = t128x16 (default) | t256x8 | t256x16
+// Tuning knob (benchmarking only): DFX_GAE_VARIANT = s128 (default: shared-memory tiles of 128 x 32 tokens,
+// 5 CTAs/SM) | s128b4 | s128b6 | s256 | s64 | t128x16 | t256x8 | t256x16 (register tiles of THREADS x TPT tokens)
 inline int gae_variant() {
   static const int v = [] {
     const char* e = std::getenv("DFX_GAE_VARIANT");
     if (!e) return 0;
     const std::string s(e);
-    return s == "t256x8" ? 1 : s == "t256x16" ? 2 : 0;
+    return s == "t256x8" ? 1 : s == "t256x16" ? 2 : s == "t128x16" ? 3 : s == "s256" ? 4 : s == "s64" ? 5 : s == "s128b4" ? 8
+           : s == "s128b6" ? 7 : 0;
   }();
   return v;
+}
+
+template <int THREADS, int MINB>
+void gae_launch_smem(GaeParams& p, cudaStream_t st) {
+  using L = SmemTile<THREADS>;
+  p.n_tiles = gae_tiles(p.begin, p.end - p.begin, L::TILE);
+  static thread_local int cached_dev = -1, resident = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
+    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_smem_kernel<THREADS, MINB, true>, THREADS, L::kBytes);
+    resident = sms * std::max(per_sm, 1);
+    cached_dev = dev;
+  }
+  static const int pf_env = std::getenv("DFX_GAE_PF") ? std::atoi(std::getenv("DFX_GAE_PF")) : 100;
+  p.pf_dist = (int64_t)resident * pf_env / 100;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)p.n_tiles);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap launch + loads with gae_prep_kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.whiten) cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, true>, p);
+  else cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, false>, p);
 }
 
 template <int THREADS, int TPT, int MINB>
@@ -434,7 +692,13 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
   switch (gae_variant()) {
     case 1: gae_launch_tile<256, 8, 4>(p, stream); break;
     case 2: gae_launch_tile<256, 16, 2>(p, stream); break;
-    default: gae_launch_tile<128, 16, 4>(p, stream); break;
+    case 3: gae_launch_tile<128, 16, 4>(p, stream); break;
+    case 4: gae_launch_smem<256, 2>(p, stream); break;
+    case 5: gae_launch_smem<64, 8>(p, stream); break;
+    case 6: gae_launch_smem<128, 5>(p, stream); break;
+    case 7: gae_launch_smem<128, 6>(p, stream); break;
+    case 8: gae_launch_smem<128, 4>(p, stream); break;
+    default: gae_launch_smem<128, 5>(p, stream); break;
   }
   DFX_LAUNCH_CHECK("gae_tile_kernel");
   if (whiten) {

@@ -79,22 +79,43 @@ __global__ void __launch_bounds__(256) broadcast_kernel(SlotGeom g, int64_t n_sl
 // ---------------------------------------------------------------------------
 // Fused loss
 // ---------------------------------------------------------------------------
-struct LossParams {
+// One token source of a loss call: a packed batch (its own token coordinates; pointers may be peer-mapped, e.g.
+// a partner GPU's producer batch read over NVLink) owning global slots [slot0, ...) and rollouts [roll0, ...).
+constexpr int kMaxLossSrc = 4;
+struct LossSrc {
   SlotGeom g;
-  int64_t n_slots;
-  int64_t n_records;
-  const int32_t* group_off;
-  const int32_t* roll_group;
-  const double* reward;
+  int64_t slot0, roll0;
   const float* lp;
   const float* old_lp;
   const float* ref_lp;
   const uint8_t* mask;
   const double* adv_roll_in;
   const float* adv_tok_in;
-  double* adv_roll_out;
   float* adv_tok_out;
   float* dlogp;
+};
+
+// global slot u -> (source, local slot); global rollout s -> source
+__device__ __forceinline__ int src_of_slot(const LossSrc* src, int n_src, int64_t u) {
+  int k = 0;
+  while (k + 1 < n_src && u >= src[k + 1].slot0) ++k;
+  return k;
+}
+__device__ __forceinline__ int src_of_roll(const LossSrc* src, int n_src, int64_t s) {
+  int k = 0;
+  while (k + 1 < n_src && s >= src[k + 1].roll0) ++k;
+  return k;
+}
+
+struct LossParams {
+  int n_src;
+  LossSrc src[kMaxLossSrc];
+  int64_t n_slots;
+  int64_t n_records;
+  const int32_t* group_off;   // fused GRPO (single source only)
+  const int32_t* roll_group;
+  const double* reward;
+  double* adv_roll_out;
   const double* whiten_sums;
   int whiten;
   float clip_lo, clip_hi, beta;
@@ -107,7 +128,7 @@ struct LossParams {
   const double* grp_stats; // dlogp: per loss group {N, S}
   double* part;            // [5][n_slots]
   int32_t* flags;
-  unsigned long long* ticket;  // [2] persistent-warp slot ticket, zero on entry, restored
+  unsigned long long* ticket;  // [kMaxLossSrc + 1] per-source slot tickets + finished warps; zero on entry, restored
 };
 
 // ---- per-token math ---------------------------------------------------------
@@ -265,7 +286,7 @@ __device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, in
 // mask words, kUnroll vectors per lane in flight, fused advantage broadcast,
 // clipped surrogate, KL and masked partial sums in registers (f32 per round,
 // f64 across rounds), one deterministic warp reduction per slot.
-template <int ADV, int KL, bool DLOGP, int UNROLL = 2, int MINB = 3>
+template <int ADV, int KL, bool DLOGP, int UNROLL = 2, int MINB = 3, bool MULTI = false>
 __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -294,19 +315,33 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     rstd = (float)(1.0 / sqrt(fmax(var, 0.0) + 1e-8));
   }
   double* part = p.part;
-  unsigned long long* next = p.ticket;  // [0] next slot, [1] finished warps
+  // tickets: [k] next slot of source k, [kMaxLossSrc] finished warps. Several sources (e.g. local HBM and a
+  // partner GPU's memory over NVLink) are drained concurrently: warp w starts on source w % n_src and moves to the
+  // next one when its source runs out, so the fast local slots overlap the slow remote ones.
+  unsigned long long* next = p.ticket;
+  int k = MULTI ? (int)(gwarp % p.n_src) : 0;
+  uint32_t live = (1u << p.n_src) - 1u;
 
   for (;;) {
     unsigned long long uu = 0;
-    if (lane == 0) uu = atomicAdd(next, 1ull);
-    const int64_t u = (int64_t)__shfl_sync(kFull, uu, 0);
-    if (u >= p.n_slots) break;
-
+    if (lane == 0) uu = atomicAdd(next + k, 1ull);
+    const int64_t ul = (int64_t)__shfl_sync(kFull, uu, 0);
+    const int64_t kend = MULTI ? (k + 1 < p.n_src ? p.src[k + 1].slot0 : p.n_slots) - p.src[k].slot0 : p.n_slots;
+    if (ul >= kend) {
+      if (!MULTI) break;
+      live &= ~(1u << k);
+      if (!live) break;
+      do k = (k + 1) % p.n_src; while (!((live >> k) & 1u));
+      continue;
+    }
+    const LossSrc& S = p.src[k];
+    const int64_t u = S.slot0 + ul;
     int64_t s, t0, t1;
-    if (!slot_unit(p.g, u, lane, s, t0, t1)) {
+    if (!slot_unit(S.g, u - S.slot0, lane, s, t0, t1)) {
       if (lane < 5) part[(int64_t)lane * p.n_slots + u] = 0.0;
       continue;
     }
+    const int64_t sg = S.roll0 + s;  // global rollout (loss groups, dlogp weights)
     float A_unit = 0.0f;
     if (ADV == DFX_ADV_GROUP_FUSED) {
       const int32_t grp = __ldg(p.roll_group + s);
@@ -314,7 +349,7 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
                                              p.adv_eps, lane);
       A_unit = (float)group_adv(__ldg(p.reward + s), gs);
     } else if (ADV == DFX_ADV_ROLLOUT) {
-      A_unit = (float)__ldg(p.adv_roll_in + s);
+      A_unit = (float)S.adv_roll_in[s];
     }
     if (ADV != DFX_ADV_TOKEN) A_unit = (A_unit - mu) * rstd;  // identity unless whitening
     const UnitAdv ua = unit_adv(A_unit, 1.0f - p.clip_lo, 1.0f + p.clip_hi);
@@ -322,22 +357,24 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     if (DLOGP) {
       int gi = 0;
       if (p.lgo)
-        while (gi + 1 < p.n_groups && __ldg(p.lgo + gi + 1) <= s) ++gi;
-      const double N = p.grp_stats[2 * gi], S = p.grp_stats[2 * gi + 1];
-      const double ns = p.seq_n[s];
+        while (gi + 1 < p.n_groups && __ldg(p.lgo + gi + 1) <= sg) ++gi;
+      const double N = p.grp_stats[2 * gi], Sq = p.grp_stats[2 * gi + 1];
+      const double ns = p.seq_n[sg];
       if (p.agg == DFX_AGG_TOKEN_MEAN) w = N > 0 ? (float)(1.0 / N) : 0.0f;
-      else if (p.agg == DFX_AGG_SEQ_MEAN_TOKEN_MEAN) w = (S > 0 && ns > 0) ? (float)(1.0 / (S * ns)) : 0.0f;
-      else w = S > 0 ? (float)(1.0 / S) : 0.0f;
+      else if (p.agg == DFX_AGG_SEQ_MEAN_TOKEN_MEAN) w = (Sq > 0 && ns > 0) ? (float)(1.0 / (Sq * ns)) : 0.0f;
+      else w = Sq > 0 ? (float)(1.0 / Sq) : 0.0f;
     }
 
     double dpg = 0.0, dkl = 0.0, dakl = 0.0, dclip = 0.0, dn = 0.0;
     const int64_t vbeg = t0 >> 2;
     const int32_t nvec = (int32_t)(((t1 + 3) >> 2) - vbeg);
-    const float* lp0 = p.lp + 4 * vbeg;
-    const float* ol0 = p.old_lp + 4 * vbeg;
-    const float* rf0 = p.ref_lp + 4 * vbeg;
-    const uint8_t* mk0 = p.mask + 4 * vbeg;
-    const float* ad0 = ADV == DFX_ADV_TOKEN ? p.adv_tok_in + 4 * vbeg : nullptr;
+    const float* lp0 = S.lp + 4 * vbeg;
+    const float* ol0 = S.old_lp + 4 * vbeg;
+    const float* rf0 = S.ref_lp + 4 * vbeg;
+    const uint8_t* mk0 = S.mask + 4 * vbeg;
+    const float* ad0 = ADV == DFX_ADV_TOKEN ? S.adv_tok_in + 4 * vbeg : nullptr;
+    float* const atout = S.adv_tok_out;
+    float* const dlout = S.dlogp;
     constexpr int kUnroll = UNROLL;
     for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
       float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
@@ -363,13 +400,13 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         if (t >= t0 && t + 4 <= t1) {
           loss_vec<ADV, KL, DLOGP, true>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
                                          gout);
-          if (p.adv_tok_out) store_vec<true>(p.adv_tok_out, t, t0, t1, aout);
-          if (DLOGP) store_vec<true>(p.dlogp, t, t0, t1, gout);
+          if (atout) store_vec<true>(atout, t, t0, t1, aout);
+          if (DLOGP) store_vec<true>(dlout, t, t0, t1, gout);
         } else {
           loss_vec<ADV, KL, DLOGP, false>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
                                           gout);
-          if (p.adv_tok_out) store_vec<false>(p.adv_tok_out, t, t0, t1, aout);
-          if (DLOGP) store_vec<false>(p.dlogp, t, t0, t1, gout);
+          if (atout) store_vec<false>(atout, t, t0, t1, aout);
+          if (DLOGP) store_vec<false>(dlout, t, t0, t1, gout);
         }
       }
       dpg += acc.pg;
@@ -394,23 +431,28 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
   // the last warp out restores the tickets for the next launch
   if (lane == 0) {
     __threadfence();
-    const unsigned long long done = atomicAdd(next + 1, 1ull);
+    const unsigned long long done = atomicAdd(next + kMaxLossSrc, 1ull);
     if (done == (unsigned long long)nwarps - 1) {
-      next[0] = 0ull;
-      next[1] = 0ull;
+#pragma unroll
+      for (int q = 0; q <= kMaxLossSrc; ++q) next[q] = 0ull;
     }
   }
 }
 
 // mask-count pre-pass (dlogp weights): part[4][u] = sum of mask over the slot
-__global__ void __launch_bounds__(256) mask_count_kernel(SlotGeom g, int64_t n_slots,
-                                                         const uint8_t* __restrict__ mask,
+struct MaskCountParams {
+  int n_src;
+  LossSrc src[kMaxLossSrc];
+};
+__global__ void __launch_bounds__(256) mask_count_kernel(MaskCountParams mp, int64_t n_slots,
                                                          double* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (u >= n_slots) return;
+  const LossSrc& S = mp.src[src_of_slot(mp.src, mp.n_src, u)];
+  const uint8_t* mask = S.mask;
   int64_t s, t0, t1;
-  if (!slot_unit(g, u, lane, s, t0, t1)) {
+  if (!slot_unit(S.g, u - S.slot0, lane, s, t0, t1)) {
     if (lane == 0) cnt[u] = 0.0;
     return;
   }
@@ -435,7 +477,9 @@ constexpr int kFinThreads = 256;
 constexpr int kFinSeqPerThread = 1;
 
 struct FinParams {
-  SlotGeom g;
+  int n_src;
+  LossSrc src[kMaxLossSrc];
+  int64_t n_roll;         // total rollouts over the sources
   int64_t n_slots;
   int n_groups;
   const int32_t* lgo;
@@ -477,17 +521,19 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
   __shared__ bool is_last;
   const int gi = blockIdx.y;
   const int64_t sr0 = f.lgo ? f.lgo[gi] : 0;
-  const int64_t sr1 = f.lgo ? f.lgo[gi + 1] : f.g.n_seq;
+  const int64_t sr1 = f.lgo ? f.lgo[gi + 1] : f.n_roll;
   double acc[6] = {0, 0, 0, 0, 0, 0};  // pg, kl, clip, akl, n, S
   const int64_t first = sr0 + (int64_t)blockIdx.x * kFinThreads * kFinSeqPerThread;
 #pragma unroll
   for (int j = 0; j < kFinSeqPerThread; ++j) {
     const int64_t s = first + (int64_t)j * kFinThreads + threadIdx.x;
     if (s >= sr1) break;
-    const int64_t a = f.g.cu[s], b = f.g.cu[s + 1];
+    const LossSrc& S = f.src[src_of_roll(f.src, f.n_src, s)];
+    const int64_t sl = s - S.roll0;
+    const int64_t a = S.g.cu[sl], b = S.g.cu[sl + 1];
     double q[5] = {0, 0, 0, 0, 0};
     if (b > a) {
-      const int64_t u0 = s + ((a - f.g.base) >> f.g.sh), u1 = s + ((b - 1 - f.g.base) >> f.g.sh);
+      const int64_t u0 = S.slot0 + sl + ((a - S.g.base) >> S.g.sh), u1 = S.slot0 + sl + ((b - 1 - S.g.base) >> S.g.sh);
       for (int64_t u = u0; u <= u1; ++u) {
         if (COUNTS) {
           q[4] += f.part[u];
@@ -572,9 +618,8 @@ struct LossWs {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t span, int32_t n_groups) {
+LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t n_slots, int32_t n_groups) {
   LossWs w{};
-  const int64_t n_slots = slot_count(n_seq, span, slot_shift(span));
   w.nb = (int)std::max<int64_t>(1, (n_seq + kFinThreads * kFinSeqPerThread - 1) / (kFinThreads * kFinSeqPerThread));
   size_t off = 0;
   char* b = static_cast<char*>(base);
@@ -586,7 +631,7 @@ LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t span, int32_t n_groups)
   // ticket first: callers zero the workspace once at allocation, and the
   // kernels restore it to zero on exit
   w.ticket = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * 2 * size_t(n_groups)));
-  w.slot_ticket = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2));
+  w.slot_ticket = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (kMaxLossSrc + 1)));
   w.part = reinterpret_cast<double*>(take(sizeof(double) * 5 * size_t(n_slots)));
   w.blk = reinterpret_cast<double*>(take(sizeof(double) * 6 * size_t(n_groups) * size_t(w.nb)));
   w.seq_n = reinterpret_cast<double*>(take(sizeof(double) * size_t(n_seq + 1)));
@@ -617,7 +662,9 @@ void launch_variant(const LossParams& p, cudaStream_t st) {
     cached_blocks = sms * std::max(per_sm, 1);
     cached_dev = dev;
   }
-  loss_slots_kernel<ADV, KL, DL, U, MB><<<cached_blocks, 256, 0, st>>>(p);
+  // a single source keeps the source index a compile-time 0 (no dynamic parameter indexing)
+  if (p.n_src > 1) loss_slots_kernel<ADV, KL, DL, U, MB, true><<<cached_blocks, 256, 0, st>>>(p);
+  else loss_slots_kernel<ADV, KL, DL, U, MB, false><<<cached_blocks, 256, 0, st>>>(p);
 }
 
 // Tuning knob (benchmarking only): DFX_LOSS_VARIANT=u2b3 (default) | u3b2 | u4b2 | u2b2 selects the
@@ -634,6 +681,12 @@ inline int loss_variant() {
 
 template <int ADV, int KL, bool DL>
 void launch_slots(const LossParams& p, cudaStream_t st) {
+  if (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL && p.n_src > 1) {
+    // sources read over NVLink have ~2x the latency of local HBM: more vectors in flight per lane
+    static const int mu = std::getenv("DFX_LOSS_MULTI_UNROLL") ? std::atoi(std::getenv("DFX_LOSS_MULTI_UNROLL")) : 4;
+    if (mu == 4) return launch_variant<ADV, KL, DL, 4, 2>(p, st);
+    if (mu == 3) return launch_variant<ADV, KL, DL, 3, 2>(p, st);
+  }
   if (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL) {
     switch (loss_variant()) {
       case 1: return launch_variant<ADV, KL, DL, 3, 2>(p, st);
@@ -701,45 +754,84 @@ dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream s
 
 size_t dfx_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span, int32_t n_loss_groups) {
   if (n_loss_groups < 1) n_loss_groups = 1;
-  return loss_ws_layout(nullptr, n_rollouts, token_span, n_loss_groups).bytes;
+  return loss_ws_layout(nullptr, n_rollouts, slot_count(n_rollouts, token_span, slot_shift(token_span)),
+                        n_loss_groups).bytes;
 }
 
-dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span, const dfx_loss_cfg* cfg,
-                        const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
-  if (!b || !cfg || !args || !args->out) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
-  if (b->n_rollouts <= 0) {
-    DFX_CUDA(cudaMemsetAsync(args->out, 0, sizeof(dfx_loss_out) * (args->n_loss_groups < 1 ? 1 : args->n_loss_groups), stream));
+size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_src, int32_t n_loss_groups) {
+  if (n_loss_groups < 1) n_loss_groups = 1;
+  int64_t S = 0, U = 0;
+  for (int32_t k = 0; srcs && k < n_src; ++k) {
+    S += srcs[k].b.n_rollouts;
+    U += slot_count(srcs[k].b.n_rollouts, srcs[k].token_span, slot_shift(srcs[k].token_span));
+  }
+  return loss_ws_layout(nullptr, S, U, n_loss_groups).bytes;
+}
+
+}  // extern "C"
+
+namespace {
+
+dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
+                         const dfx_loss_args* args, void* workspace, size_t ws_bytes, cudaStream_t stream) {
+  if (!srcs || n_src < 1 || !cfg || !args || !args->out) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
+  if (n_src > kMaxLossSrc) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: at most 4 sources");
+  const int32_t ng = args->n_loss_groups < 1 ? 1 : args->n_loss_groups;
+  int64_t S = 0, U = 0;
+  for (int32_t k = 0; k < n_src; ++k) S += srcs[k].b.n_rollouts;
+  if (S <= 0) {
+    DFX_CUDA(cudaMemsetAsync(args->out, 0, sizeof(dfx_loss_out) * ng, stream));
     return DFX_OK;
   }
-  if (!b->cu_seqlens || !b->lp || !b->old_lp || !b->ref_lp || !b->mask)
-    return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: packed batch lacks cu_seqlens/lp/old_lp/ref_lp/mask");
-  const int32_t ng = args->n_loss_groups < 1 ? 1 : args->n_loss_groups;
   if (ng > 1 && !args->loss_group_off) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: loss_group_off required for >1 group");
-  switch (cfg->adv_source) {
-    case DFX_ADV_GROUP_FUSED:
-      if (!b->reward) return fail(DFX_MISSING_CHANNEL, "missing channel 'reward'");
-      if (!b->group_off || !b->roll_group) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: fused GRPO needs group_off/roll_group");
-      break;
-    case DFX_ADV_ROLLOUT:
-      if (!args->adv_roll) return fail(DFX_MISSING_CHANNEL, "missing channel 'advantage'");
-      break;
-    case DFX_ADV_TOKEN:
-      if (!args->adv_tok_in) return fail(DFX_MISSING_CHANNEL, "missing per-token advantage");
-      break;
-    default:
-      return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad adv_source");
-  }
+  if (cfg->adv_source == DFX_ADV_GROUP_FUSED && n_src != 1)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: the fused GRPO advantage needs a single source");
   if (cfg->whiten && !args->whiten_sums) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: whiten needs whiten_sums");
   if (cfg->kl_type < 0 || cfg->kl_type > 3 || cfg->agg < 0 || cfg->agg > 2) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad kl_type/agg");
-  const int64_t S = b->n_rollouts;
-  const LossWs w = loss_ws_layout(workspace, S, token_span, ng);
+  bool want_dl = false;
+  LossSrc src[kMaxLossSrc] = {};
+  for (int32_t k = 0; k < n_src; ++k) {
+    const dfx_loss_src& x = srcs[k];
+    const dfx_packed* b = &x.b;
+    if (b->n_rollouts > 0 && (!b->cu_seqlens || !b->lp || !b->old_lp || !b->ref_lp || !b->mask))
+      return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: packed batch lacks cu_seqlens/lp/old_lp/ref_lp/mask");
+    switch (cfg->adv_source) {
+      case DFX_ADV_GROUP_FUSED:
+        if (!b->reward) return fail(DFX_MISSING_CHANNEL, "missing channel 'reward'");
+        if (!b->group_off || !b->roll_group) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: fused GRPO needs group_off/roll_group");
+        break;
+      case DFX_ADV_ROLLOUT:
+        if (!x.adv_roll && b->n_rollouts > 0) return fail(DFX_MISSING_CHANNEL, "missing channel 'advantage'");
+        break;
+      case DFX_ADV_TOKEN:
+        if (!x.adv_tok_in && b->n_rollouts > 0) return fail(DFX_MISSING_CHANNEL, "missing per-token advantage");
+        break;
+      default:
+        return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad adv_source");
+    }
+    if (k > 0 && (x.dlogp != nullptr) != want_dl) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: dlogp on all sources or none");
+    want_dl = x.dlogp != nullptr;
+    src[k].g = geom_of(b, x.token_base & ~int64_t(3), x.token_span);
+    src[k].slot0 = U;
+    src[k].roll0 = k == 0 ? 0 : src[k - 1].roll0 + srcs[k - 1].b.n_rollouts;
+    src[k].lp = b->lp;
+    src[k].old_lp = b->old_lp;
+    src[k].ref_lp = b->ref_lp;
+    src[k].mask = b->mask;
+    src[k].adv_roll_in = x.adv_roll;
+    src[k].adv_tok_in = x.adv_tok_in;
+    src[k].adv_tok_out = x.adv_tok_out;
+    src[k].dlogp = x.dlogp;
+    U += slot_count(b->n_rollouts, x.token_span, slot_shift(x.token_span));
+  }
+  const LossWs w = loss_ws_layout(workspace, S, U, ng);
   if (!workspace || ws_bytes < w.bytes) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: workspace too small");
-  const SlotGeom g = geom_of(b, token_base & ~int64_t(3), token_span);
-  const int64_t n_slots = slot_count(S, token_span, slot_shift(token_span));
-  const bool want_dl = args->dlogp != nullptr;
+  const int64_t n_slots = U;
 
   FinParams f{};
-  f.g = g;
+  f.n_src = n_src;
+  for (int32_t k = 0; k < n_src; ++k) f.src[k] = src[k];
+  f.n_roll = S;
   f.n_slots = n_slots;
   f.n_groups = ng;
   f.lgo = args->loss_group_off;
@@ -753,7 +845,10 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
   const dim3 fgrid((unsigned)w.nb, (unsigned)ng);
 
   if (want_dl) {
-    mask_count_kernel<<<(unsigned)((n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock), 256, 0, stream>>>(g, n_slots, b->mask, w.part);
+    MaskCountParams mp{};
+    mp.n_src = n_src;
+    for (int32_t k = 0; k < n_src; ++k) mp.src[k] = src[k];
+    mask_count_kernel<<<(unsigned)((n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock), 256, 0, stream>>>(mp, n_slots, w.part);
     DFX_LAUNCH_CHECK("mask_count_kernel");
     f.part = w.part;
     f.ticket = w.ticket + ng;
@@ -761,22 +856,16 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
     DFX_LAUNCH_CHECK("finalize_kernel<counts>");
   }
 
+  const dfx_packed* b0 = &srcs[0].b;
   LossParams p{};
-  p.g = g;
+  p.n_src = n_src;
+  for (int32_t k = 0; k < n_src; ++k) p.src[k] = src[k];
   p.n_slots = n_slots;
-  p.n_records = b->n_records;
-  p.group_off = b->group_off;
-  p.roll_group = b->roll_group;
-  p.reward = b->reward;
-  p.lp = b->lp;
-  p.old_lp = b->old_lp;
-  p.ref_lp = b->ref_lp;
-  p.mask = b->mask;
-  p.adv_roll_in = args->adv_roll;
-  p.adv_tok_in = args->adv_tok_in;
-  p.adv_roll_out = cfg->adv_source == DFX_ADV_GROUP_FUSED ? const_cast<double*>(args->adv_roll) : nullptr;
-  p.adv_tok_out = args->adv_tok_out;
-  p.dlogp = args->dlogp;
+  p.n_records = b0->n_records;
+  p.group_off = b0->group_off;
+  p.roll_group = b0->roll_group;
+  p.reward = b0->reward;
+  p.adv_roll_out = cfg->adv_source == DFX_ADV_GROUP_FUSED ? const_cast<double*>(srcs[0].adv_roll) : nullptr;
   p.whiten_sums = args->whiten_sums;
   p.whiten = cfg->whiten;
   p.clip_lo = (float)cfg->clip_low;
@@ -805,6 +894,29 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
   finalize_kernel<false><<<fgrid, kFinThreads, 0, stream>>>(f);
   DFX_LAUNCH_CHECK("finalize_kernel");
   return DFX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span, const dfx_loss_cfg* cfg,
+                        const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
+  if (!b || !args) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
+  dfx_loss_src s{};
+  s.b = *b;
+  s.token_base = token_base;
+  s.token_span = token_span;
+  s.adv_roll = args->adv_roll;
+  s.adv_tok_in = args->adv_tok_in;
+  s.adv_tok_out = args->adv_tok_out;
+  s.dlogp = args->dlogp;
+  return ppo_loss_impl(&s, 1, cfg, args, workspace, ws_bytes, stream);
+}
+
+dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
+                              const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
+  return ppo_loss_impl(srcs, n_src, cfg, args, workspace, ws_bytes, stream);
 }
 
 dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream) {

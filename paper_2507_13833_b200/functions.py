@@ -246,6 +246,58 @@ def ppo_loss(batch: PackedBatch, ctx: StageContext, adv_source: str | None = Non
     return res
 
 
+def ppo_loss_sources(sources: list, ctx: StageContext, loss_group_off=None, adv_tok_out: bool = False,
+                     events=None, device=None) -> dict:
+    """dfx_ppo_loss_multi over several token sources in order (local PackedBatch views and/or RemoteSource runs of a
+    partner GPU's producer batch, read over NVLink by the streaming kernel): the consumer side of a reshard fused
+    with the loss, no copy of the remote tokens. Advantages: each source's 'advantage' rollout channel.
+    Returns {"out": [n_groups, 7], "adv_tok": [per-source f32 tensors] (adv_tok_out)}."""
+    cfg = ctx.loss
+    if cfg.whiten or cfg.want_grad:
+        raise errors.Error("ppo_loss_sources: whitening / dlogp are single-source features")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ng = 1 if loss_group_off is None else len(loss_group_off) - 1
+    out = torch.empty(ng * 7, dtype=torch.float64, device=dev)
+    arr = (_abi.LossSrc * len(sources))()
+    keep, aouts = [], []
+    for k, src in enumerate(sources):
+        x = arr[k]
+        if isinstance(src, PackedBatch):
+            for n in ("lp", "old_lp", "ref_lp", "mask"):
+                _stream(src, n)
+            x.b = src.struct()
+            x.token_base, x.token_span = src.token_base, src.token_span
+            x.adv_roll = _ptr(_channel(src, "advantage"))
+        else:  # RemoteSource
+            x.b = src.struct()
+            x.token_base, x.token_span = src.token_base, src.token_span
+            x.adv_roll = src.addr["c:advantage"]
+        if adv_tok_out:  # a local array per source, addressed in the source's token coordinates
+            a0 = x.token_base & ~3
+            buf = torch.empty(((x.token_span + (x.token_base - a0) + 3) // 4) * 4 + 4, dtype=torch.float32,
+                              device=dev)
+            x.adv_tok_out = buf.data_ptr() - 4 * a0
+            aouts.append(buf)
+        keep.append(x.b)
+    lgo = None
+    if loss_group_off is not None:
+        key = ("lgo", tuple(int(v) for v in loss_group_off))
+        lgo = ctx.workspace.const(key, lambda: torch.as_tensor(np.asarray(loss_group_off, np.int32)).to(dev))
+    c = _abi.LossCfg(cfg.clip_low, cfg.clip_high, cfg.beta, float(ctx.advantage_eps), _abi.KL[cfg.kl],
+                     _abi.AGG[cfg.agg], _abi.ADV["rollout"], 0)
+    ev = events or (None, None)
+    a = _abi.LossArgs(None, None, None, None, None, ng, _ptr(lgo), _ptr(out), None, ev[0], ev[1])
+    L = _abi.lib()
+    nbytes = L.dfx_ppo_loss_multi_workspace_bytes(arr, len(sources), ng)
+    ws = ctx.workspace.get("loss_multi", nbytes, dev)
+    _abi.check(L.dfx_ppo_loss_multi(arr, len(sources), C.byref(c), C.byref(a), _ptr(ws), ws.numel(),
+                                    ctx.cuda_stream(dev)))
+    res = {"out": out.view(ng, 7)}
+    if adv_tok_out:
+        res["adv_tok"] = aouts
+    return res
+
+
 def loss_dict(out_row: torch.Tensor) -> dict:
     vals = out_row.detach().cpu().tolist()
     return dict(zip(_abi.LOSS_OUT_FIELDS, vals))

@@ -166,15 +166,39 @@ class Plan:
 
 
 @dataclass
+class RemoteSource:
+    """A run of consecutive records of a producer batch held by another GPU, mapped into this GPU's address space
+    (CUDA IPC over NVLink): device addresses of the run's first ids / group_off / cu_seqlens / channel entries and
+    the base addresses of the token streams (absolute token coordinates, like the producer's own cu_seqlens).
+    Kernels read it in place over NVLink; nothing is copied."""
+    rank: int
+    n_records: int
+    n_rollouts: int
+    token_base: int
+    token_span: int
+    addr: dict
+
+    def struct(self) -> _abi.Packed:
+        a = self.addr
+        return _abi.Packed(self.n_records, self.n_rollouts, a.get("group_off"), None, a.get("cu"), a.get("c:reward"),
+                           a.get("c:value"), a.get("s:lp"), a.get("s:old_lp"), a.get("s:ref_lp"), a.get("s:value_tok"),
+                           a.get("s:token_reward"), a.get("s:mask"))
+
+
+@dataclass
 class ConsumerBatch:
-    """This rank's consumer groups, concatenated in dp order, with per-group record/rollout offsets."""
-    batch: PackedBatch
+    """This rank's consumer groups, concatenated in dp order, with per-group record/rollout offsets. A lazy
+    exchange (exchange(..., lazy=True)) has batch None and, per group, the token sources in order: local
+    PackedBatch views and RemoteSource runs on peer GPUs; release() must follow its last use (device barrier)."""
+    batch: PackedBatch | None
     groups: list            # consumer dp ranks held here, in order
     rec_off: list           # record offsets per group (len(groups)+1)
     roll_off: list          # rollout offsets per group
     zero_copy: bool
     bytes_sent: int = 0
     bytes_recv: int = 0
+    sources: list | None = None   # lazy: per group, [PackedBatch | RemoteSource]
+    release: object = None        # lazy: callable issuing the closing device barrier
 
     def group_view(self, d: int) -> PackedBatch:
         i = self.groups.index(d)
@@ -219,7 +243,7 @@ def _src_slices(plan: Plan, sources: dict):
 
 
 def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, meta_group=None,
-             transport: str = "pull") -> ConsumerBatch:
+             transport: str = "pull", lazy: bool = False) -> ConsumerBatch:
     """Run the reshard on this rank. sources: {producer dp rank: (PackedBatch, first record of that group in it)}
     for every locally held producer group. schema: (stream name -> dtype, channel names), needed only on ranks
     that hold no producer group. Collective across the ranks of `group` (torch.distributed NCCL group) when
@@ -228,7 +252,10 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     transport "pull" (default): consumers map the producers' buffers (CUDA IPC, dfx_ipc_export/open) and pull the
     token ranges over NVLink with copy engines; the unpack kernel reads the producers' record metadata straight
     from peer memory; two device-side NCCL barriers order the pulls against production and reuse.
-    transport "nccl": grouped NCCL send/recv of 16-aligned token ranges + packed metadata (dfx_reshard_pack)."""
+    transport "nccl": grouped NCCL send/recv of 16-aligned token ranges + packed metadata (dfx_reshard_pack).
+    lazy (pull transport): no consumer batch is built; remote segments stay in the producers' memory as
+    RemoteSource runs that the consumer's kernels read over NVLink (dfx_ppo_loss_multi), local segments are views.
+    The caller runs ConsumerBatch.release() after its last read (the second device barrier)."""
     L = _declare()
     rank = plan.rank
     for p in plan.local_src:
@@ -291,6 +318,31 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
                 return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0)
             _, sent, recv_b, _ = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)
             return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, recv_b)
+
+    if lazy and pull:
+        _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+        per_group = []
+        for d in groups:
+            srcs = []
+            for i in seg_of[d]:
+                if i in loc:
+                    b, r0, r1, s0, s1, t0, t1 = loc[i]
+                    srcs.append(b.view_records(r0, r1))
+                    continue
+                n_roll, n_tok, _, t0, s0, r0 = (int(x) for x in sizes[i])
+                src = plan.src_rank[plan.segs[i][1]]
+                pa = peer_addr[(src, plan.segs[i][1])]
+                addr = {"ids": pa["ids"] + 8 * r0, "group_off": pa["group_off"] + 4 * r0, "cu": pa["cu"] + 8 * s0}
+                for name in ch_names:
+                    addr["c:" + name] = pa["c:" + name] + 8 * s0
+                for k in stream_specs:
+                    addr["s:" + k] = pa["s:" + k]
+                srcs.append(RemoteSource(src, int(plan.segs[i][4]), n_roll, t0, n_tok, addr))
+            per_group.append(srcs)
+        recv_b = sum(int(sizes[i, 1]) * sum(torch.empty(0, dtype=dt_).element_size() for dt_ in stream_specs.values())
+                     for i in order if i not in loc)
+        return ConsumerBatch(None, groups, rec_off, roll_off, False, 0, recv_b, per_group,
+                             release=lambda: _device_barrier(group, dev))
 
     # 3. allocate the consumer batch
     R, S, T = rec_off[-1], roll_off[-1], tok_off[-1]

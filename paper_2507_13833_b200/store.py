@@ -73,7 +73,7 @@ class DeviceBufferStore:
         e.by_group[dp_rank] = batch
         return True
 
-    def ensure_ready(self, stage: str, iteration: int, fallback_to_layout: Layout) -> ConsumerBatch:
+    def ensure_ready(self, stage: str, iteration: int, fallback_to_layout: Layout, lazy: bool = False) -> ConsumerBatch:
         sp = self._plan(stage)
         self._stale("get", iteration)
         to = sp.consumed or fallback_to_layout
@@ -92,7 +92,7 @@ class DeviceBufferStore:
         plan = Plan(self.topo, sp.produced, to, counts, self.rank)
         sources = {p: (e.by_group[p], 0) for p in local}
         e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
-                           transport=self.transport)
+                           transport=self.transport, lazy=lazy)
         e.consumed = to
         e.by_group = {}
         self.bytes_sent += e.ready.bytes_sent
@@ -113,6 +113,8 @@ class DeviceBufferStore:
 
     def get(self, stage: str, iteration: int, dest_dp_rank: int, to_layout: Layout) -> PackedBatch:
         ready = self.ensure_ready(stage, iteration, to_layout)
+        if ready.batch is None:
+            raise errors.Error("get() after a lazy ensure_ready: the consumer batch is mapped, not materialized")
         if dest_dp_rank not in ready.groups:
             raise errors.Error(f"dp group {dest_dp_rank} not local to rank {self.rank}")
         return ready.group_view(dest_dp_rank)
@@ -123,6 +125,10 @@ class DeviceBufferStore:
             self._done[iteration] = c
             return
         self._done.pop(iteration, None)
+        for k, e in self._entries.items():  # lazy consumers: peers may reuse their buffers after this barrier
+            if k[1] <= iteration and e.ready is not None and e.ready.release is not None:
+                e.ready.release()
+                e.ready.release = None
         self.low_water = max(self.low_water, iteration + 1)
         self._entries = {k: v for k, v in self._entries.items() if k[1] >= self.low_water}
 

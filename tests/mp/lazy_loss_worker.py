@@ -1,0 +1,63 @@
+"""torchrun worker (2 GPUs): the lazy reshard + fused multi-source loss == materialize-then-loss.
+
+Box placement with W = 2 logical workers on 2 GPUs: producer dp 2 (tp 1), consumer dp 1 (tp 2), so the one
+consumer group's TP workers sit on different GPUs and each GPU needs its partner's producer group. The lazy path
+maps the partner's batch (CUDA IPC) and the loss kernel reads it over NVLink in place; the reference path pulls it
+into a local consumer batch first. Losses must agree to f32 partial-sum rounding (the slot windows differ), per-token
+advantages bit-exactly.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import paper_2507_13833_b200 as dfx  # noqa: E402
+from paper_2507_13833_b200.reshard import Layout, RemoteSource, Topology  # noqa: E402
+from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan  # noqa: E402
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dev = torch.device("cuda", rank)
+dist.init_process_group("nccl", device_id=dev)
+meta = dist.new_group(backend="gloo")
+R = 48
+for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("uniform", 37))):
+    b = dfx.PackedBatch.synthetic(5 + it, R, 4, dfx.TokenDist(dist_kind, 0, 1, hi), device=dev, first_id=rank * R)
+    ctx = dfx.StageContext()
+    dfx.fn_group_advantage(dfx.NodeSpec("adv"), b, ctx)
+    topo = Topology.box(2, world)
+    plan = {"s": StoreStagePlan(Layout(2, 1), Layout(1, 2))}
+    lazy_store = DeviceBufferStore(topo, rank, plan, meta_group=meta)
+    ref_store = DeviceBufferStore(topo, rank, plan, meta_group=meta)
+    lazy_store.put("s", it, rank, 0, b)
+    ref_store.put("s", it, rank, 0, b)
+    cb = lazy_store.ensure_ready("s", it, Layout(1, 2), lazy=True)
+    assert cb.sources is not None and len(cb.sources) == 1
+    srcs = cb.sources[0]
+    assert [isinstance(x, RemoteSource) for x in srcs] == [rank == 1, rank == 0], srcs
+    res = dfx.ppo_loss_sources(srcs, ctx, loss_group_off=cb.roll_off, adv_tok_out=True, device=dev)
+    got = res["out"].cpu().numpy()[0]
+    lazy_store.worker_done(it)
+    rb = ref_store.ensure_ready("s", it, Layout(1, 2))
+    ref = dfx.ppo_loss(rb.batch, dfx.StageContext(), adv_source="rollout", adv_tok_out=True)
+    want = ref["out"].cpu().numpy()[0]
+    assert got[5] == want[5] and got[6] == want[6], (got, want)  # token / sequence counts exact
+    # f32 partial sums over different slot windows (each source keeps its own token coordinates): f32 rounding
+    np.testing.assert_allclose(got[:5], want[:5], rtol=2e-6, atol=1e-9)
+    # per-token advantages: source k's tokens land at the consumer's cumulative token offset
+    want_tok = ref["adv_tok"].cpu().numpy()
+    off = 0
+    for x, buf in zip(srcs, res["adv_tok"]):
+        a0 = x.token_base & ~3
+        gt = buf.cpu().numpy()[x.token_base - a0: x.token_base - a0 + x.token_span]
+        assert gt.tobytes() == want_tok[off: off + x.token_span].tobytes(), (it, rank)
+        off += x.token_span
+    print(f"rank {rank} case {it}: loss {got[0]:.9f} == {want[0]:.9f}, {int(got[5])} tokens", flush=True)
+dist.barrier()
+print("LAZY_OK", flush=True)
+dist.destroy_process_group()

@@ -226,3 +226,18 @@ def test_two_gpu_nccl_reshard():
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("RESHARD_OK") == 2, r.stdout[-2000:]
+
+
+@pytest.mark.gpu
+def test_two_gpu_lazy_reshard_fused_loss():
+    """TP partners on different GPUs: the loss kernel reading the partner's records over NVLink in place equals
+    the loss over the materialized consumer batch (tests/mp/lazy_loss_worker.py)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    port = 29100 + (os.getpid() % 500)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "mp", "lazy_loss_worker.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("LAZY_OK") == 2, r.stdout[-2000:]
