@@ -39,6 +39,7 @@ C2 = dict(records=1024, n_roll=16, dist=("uniform", 0, 1, 4096), seed=1)
 C5 = dict(records=4096, n_roll=16, dist=("skewed", 0, 1, 16384), seed=11)
 BYTES_PER_TOKEN = 17      # lp, old_lp, ref_lp (3x4) + mask (1) + advantage write (4)
 BYTES_PER_ROLLOUT = 16    # f64 advantage read + i64 cu_seqlens read
+NVLINK_PEER_GBS = 770.0   # measured peer copy per direction (/opt/skills/guides/B200_PROFILING.md)
 
 
 def parse():
@@ -196,6 +197,14 @@ class DagSlice:
         self.last = cb
         return res, cb.batch
 
+    def remote_sources(self):
+        """The partner-GPU runs the last step's loss read over NVLink (lazy exchange), else []."""
+        from paper_2507_13833_b200.reshard import RemoteSource
+        cb = self.last
+        if cb is None or cb.sources is None:
+            return []
+        return [x for grp in cb.sources for x in grp if isinstance(x, RemoteSource)]
+
     def launches_per_step(self):
         # grpo_adv + loss_slots + finalize; records crossing GPUs: + the materializing unpack kernel (lazy: none,
         # the loss kernel reads the partner's records over NVLink)
@@ -321,11 +330,24 @@ def run_dfx(args):
     bytes_launch = tokens_local * BYTES_PER_TOKEN + batch.n_rollouts * BYTES_PER_ROLLOUT
     peak, peak_src = measured_peak_hbm()
     roof = None
-    if kern:
+    remote = resh.remote_sources()
+    if kern and remote:
+        # TP partners on different GPUs: the loss kernel streams the local group from HBM and the partner's group
+        # over NVLink; the NVLink half bounds it. Bytes crossing NVLink per launch: the partner's lp/old/ref/mask
+        # (13 B/token) + its advantage and cu_seqlens (16 B/rollout).
+        nv = sum(x.token_span * 13 + x.n_rollouts * 16 for x in remote)
+        local_b = bytes_launch
+        ach = nv / (kern / 1e3) / 1e9
+        roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "frac": round(ach / NVLINK_PEER_GBS, 4), "traffic": None,
+                "kernel": "dfx::loss_slots_kernel (multi-source: local HBM + partner GPU over NVLink)",
+                "kernel_ms": round(kern, 5), "bytes_per_launch": nv, "hbm_bytes_per_launch": local_b,
+                "peak_source": "measured peer copy, 770 GB/s per direction (B200_PROFILING.md)"}
+    elif kern:
         ach = bytes_launch / (kern / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(), "kernel": "dfx::loss_slots_kernel", "kernel_ms": round(kern, 5),
-                "bytes_per_launch": bytes_launch, "peak_source": peak_src}
+                "traffic": ncu_traffic() if args.workload == "c2" else None, "kernel": "dfx::loss_slots_kernel",
+                "kernel_ms": round(kern, 5), "bytes_per_launch": bytes_launch, "peak_source": peak_src}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -136,12 +136,23 @@ def _stream(batch: PackedBatch, name: str) -> torch.Tensor:
     return t
 
 
+def _reuse_channel(batch: PackedBatch, name: str) -> torch.Tensor:
+    """The f64 rollout channel to (over)write: the batch's existing one when it is its own storage of the right
+    shape (a stable address for peers that map it), else a fresh tensor. The reference overwrites the channel the
+    same way (functions.hpp:159, :170)."""
+    t = batch.channels.get(name)
+    if t is not None and t.dtype == torch.float64 and t.numel() == batch.n_rollouts and t.is_contiguous() \
+            and t.device == batch.device and (batch.parent is None or name not in batch.parent.channels):
+        return t
+    return torch.empty(batch.n_rollouts, dtype=torch.float64, device=batch.device)
+
+
 # ---- stage functions ------------------------------------------------------------------------
 def fn_group_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
     """GPU fn_group_advantage (functions.hpp:143-161): f64, bit-identical; writes channel 'advantage'."""
     _require_rollouts(batch)
     _channel(batch, "reward")
-    adv = torch.empty(batch.n_rollouts, dtype=torch.float64, device=batch.device)
+    adv = _reuse_channel(batch, "advantage")
     st = batch.struct()
     _abi.check(_abi.lib().dfx_grpo_advantage(C.byref(st), float(ctx.advantage_eps), _ptr(adv), None,
                                              ctx.cuda_stream(batch.device)))
@@ -153,7 +164,7 @@ def fn_ppo_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
     _require_rollouts(batch)
     _channel(batch, "reward")
     _channel(batch, "value")
-    adv = torch.empty(batch.n_rollouts, dtype=torch.float64, device=batch.device)
+    adv = _reuse_channel(batch, "advantage")
     st = batch.struct()
     _abi.check(_abi.lib().dfx_ppo_advantage(C.byref(st), _ptr(adv), ctx.cuda_stream(batch.device)))
     batch.channels["advantage"] = adv

@@ -429,6 +429,15 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     return ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
 
 
+def reuse_lazy(prev: ConsumerBatch, group) -> ConsumerBatch:
+    """A lazy consumer batch for a step whose producer batches are the ones `prev` mapped (same memory and
+    extents on every rank, checked by the store): same sources, fresh ordering barriers."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+    return ConsumerBatch(None, prev.groups, prev.rec_off, prev.roll_off, False, prev.bytes_sent, prev.bytes_recv,
+                         prev.sources, release=lambda: _device_barrier(group, dev))
+
+
 _BARRIER = {}
 
 

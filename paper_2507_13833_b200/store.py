@@ -18,7 +18,24 @@ from dataclasses import dataclass, field
 
 from . import errors
 from .packed import PackedBatch
-from .reshard import ConsumerBatch, Layout, Plan, Topology, exchange
+from .reshard import ConsumerBatch, Layout, Plan, Topology, exchange, reuse_lazy
+
+
+def _signature(batches) -> int:
+    """A 63-bit digest of what a lazy exchange reads from this rank's producer batches: device addresses of every
+    array, extents, and a checksum of the host offsets. Equal digests on every rank => last step's mapping holds."""
+    import numpy as np
+
+    h = []
+    for b in batches:
+        root = b.parent if b.parent is not None else b
+        arrs = [root.ids, root.cu_seqlens] + [root.channels[k] for k in sorted(root.channels)] + \
+               [root.streams[k] for k in sorted(root.streams)]
+        h += [t.data_ptr() for t in arrs] + [b.n_records, b.n_rollouts, b.token_base, b.token_span, b.parent_rec]
+        b.ensure_host_meta()
+        w = np.arange(len(b.host_cu), dtype=np.int64) % 1021 + 1
+        h += [int(np.dot(b.host_cu, w)), int(np.dot(b.host_group_off, w[:len(b.host_group_off)]))]
+    return hash(tuple(h)) & 0x7FFFFFFFFFFFFFFF
 
 
 @dataclass
@@ -44,6 +61,9 @@ class DeviceBufferStore:
         self.local_workers = [w for w in range(topo.world) if topo.gpu_of_worker[w] == rank]
         self._entries: dict = {}
         self._done: dict = {}
+        self._plans: dict = {}       # (stage, consumed layout, counts) -> Plan
+        self._templates: dict = {}   # stage -> (key, lazy ConsumerBatch) for reuse when nothing changed
+        self.template_hits = 0
         self.low_water = 0
         self.suppressed = 0
         self.bytes_sent = 0
@@ -87,29 +107,53 @@ class DeviceBufferStore:
             raise errors.NotReadyError(f"stage '{stage}' iteration {iteration} not ready: {len(missing)} puts "
                                        "outstanding")
         counts = [e.by_group[p].n_records if p in e.by_group else 0 for p in range(sp.produced.dp)]
-        # every rank must agree on the producer group sizes; ranks only know their own -> the plan needs them
-        counts = self._agree_counts(counts, local)
-        plan = Plan(self.topo, sp.produced, to, counts, self.rank)
+        # every rank must agree on the producer group sizes; ranks only know their own -> the plan needs them.
+        # One small host all-gather carries the counts and a signature of every rank's producer batches.
+        sig = _signature([e.by_group[p] for p in local]) if lazy else 0
+        counts, sigs = self._agree_counts(counts, local, sig)
+        pkey = (stage, to, tuple(counts))
+        plan = self._plans.get(pkey)
+        if plan is None:
+            plan = self._plans[pkey] = Plan(self.topo, sp.produced, to, counts, self.rank)
         sources = {p: (e.by_group[p], 0) for p in local}
-        e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
-                           transport=self.transport, lazy=lazy)
+        tkey = (pkey, tuple(sigs))
+        tmpl = self._templates.get(stage)
+        if lazy and tmpl is not None and tmpl[0] == tkey:
+            # same producer batches everywhere as last time (same memory, same extents): reuse the mapped
+            # consumer sources, no table exchange -- only the ordering barrier
+            e.ready = reuse_lazy(tmpl[1], self.group)
+            self.template_hits += 1
+        else:
+            e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
+                               transport=self.transport, lazy=lazy)
+            if lazy and e.ready.sources is not None:
+                self._templates[stage] = (tkey, e.ready)
         e.consumed = to
         e.by_group = {}
         self.bytes_sent += e.ready.bytes_sent
         self.bytes_recv += e.ready.bytes_recv
         return e.ready
 
-    def _agree_counts(self, counts, local):
-        """Producer group record counts are known only to their owners; every rank needs all of them."""
+    def _agree_counts(self, counts, local, sig=0):
+        """Producer group record counts are known only to their owners; every rank needs all of them. Returns
+        (counts, per-rank signatures) from one all-gather (CPU group when available)."""
         import numpy as np
         import torch
+        import torch.distributed as dist
 
-        from .reshard import _distributed, all_reduce_host
+        from .reshard import _distributed
         if not _distributed(self.group):
-            return counts
-        mine = np.array([c if p in local else 0 for p, c in enumerate(counts)], np.int64)
-        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
-        return all_reduce_host(mine, self.group, self.meta_group, dev).tolist()
+            return counts, [sig]
+        mine = np.array([c if p in local else 0 for p, c in enumerate(counts)] + [sig], np.int64)
+        t = torch.from_numpy(mine)
+        g = self.meta_group
+        if g is None:
+            t = t.to(torch.device("cuda", torch.cuda.current_device()))
+            g = self.group
+        parts = [torch.empty_like(t) for _ in range(dist.get_world_size(g))]
+        dist.all_gather(parts, t, group=g)
+        rows = np.stack([x.cpu().numpy() for x in parts])
+        return rows[:, :-1].sum(axis=0).tolist(), rows[:, -1].tolist()
 
     def get(self, stage: str, iteration: int, dest_dp_rank: int, to_layout: Layout) -> PackedBatch:
         ready = self.ensure_ready(stage, iteration, to_layout)

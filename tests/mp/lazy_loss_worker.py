@@ -57,6 +57,14 @@ for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("unif
         gt = buf.cpu().numpy()[x.token_base - a0: x.token_base - a0 + x.token_span]
         assert gt.tobytes() == want_tok[off: off + x.token_span].tobytes(), (it, rank)
         off += x.token_span
+    # the next iteration over the same producer batches reuses the mapping (no table exchange): same result
+    dfx.fn_group_advantage(dfx.NodeSpec("adv"), b, ctx)
+    lazy_store.put("s", it + 100, rank, 0, b)
+    cb2 = lazy_store.ensure_ready("s", it + 100, Layout(1, 2), lazy=True)
+    assert lazy_store.template_hits == 1 and cb2.sources is cb.sources
+    again = dfx.ppo_loss_sources(cb2.sources[0], ctx, loss_group_off=cb2.roll_off, device=dev)["out"]
+    assert again.cpu().numpy().tobytes() == res["out"].cpu().numpy().tobytes()
+    lazy_store.worker_done(it + 100)
     print(f"rank {rank} case {it}: loss {got[0]:.9f} == {want[0]:.9f}, {int(got[5])} tokens", flush=True)
 dist.barrier()
 print("LAZY_OK", flush=True)

@@ -106,7 +106,8 @@ def _gloo_worker(rank, world, port, q):
         full = [0] * 4
         for j in range(2):
             full[2 * rank + j] = counts[j]
-        agreed = st._agree_counts(full, [2 * rank, 2 * rank + 1])
+        agreed, sigs = st._agree_counts(full, [2 * rank, 2 * rank + 1], 7 + rank)
+        assert sigs == [7, 8]                                 # every rank sees every rank's batch signature
         plan = R.Plan(topo, R.Layout(4, 1), R.Layout(2, 2), [4, 4, 4, 4], rank)
         sends = sorted((i, r) for i, (d, p, *_r) in enumerate(plan.segs) for r in plan.dst_ranks[d]
                        if plan.src_rank[p] == rank and r != rank)
