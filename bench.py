@@ -213,6 +213,9 @@ class DagSlice:
     def describe(self):
         if not self.cross:
             mode = "zero-copy views: every consumer group's TP workers and producer groups share a GPU"
+        elif self.lazy and self.placement == "store":
+            mode = ("records cross GPUs (dense slice/exchange/concat): each consumer maps the remote slices (CUDA "
+                    "IPC) and the loss kernel streams them over NVLink in place (dfx_ppo_loss_multi), no copy")
         elif self.lazy:
             mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC) and the "
                     "loss kernel streams it over NVLink in place (dfx_ppo_loss_multi), no copy")

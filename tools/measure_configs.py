@@ -1,7 +1,8 @@
 """Per-config kernel timings (CUDA events, warm, inputs resident in HBM) for BASELINE.json's configs.
 
 usage: python tools/measure_configs.py [--out profiles/r01_configs.json]
-C1 GRPO 64x8x1024 dense; C2 GRPO 1024x16xU[1,4096]; C3 PPO 512x8192 (GAE + whitening + clipped loss);
+C1 GRPO 64x8x1024 dense; C2 GRPO 1024x16xU[1,4096]; C3 PPO 512x8192 (GAE + whitening + clipped loss, timed as
+CUDA-graph replays: the GAE call is three short launches);
 C5 GRPO per-GPU share of 4096x16 skewed <=16k at 8 GPUs (512 prompts); C4 reshard 16.8M tokens dp8->dp4->dp8
 on one GPU (logical workers; zero-copy) -- the multi-GPU reshard is measured by bench.py --gpus N.
 """
@@ -37,6 +38,31 @@ def timeit(fn, iters=30, warm=5):
     return s.elapsed_time(e) / iters
 
 
+def graph_ms(fn, reps=20):
+    """Device time per call of fn captured `reps` times in one CUDA graph (launch overhead of a real pipeline,
+    no Python in the timed region)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(5):
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e) / reps)
+    return sorted(ts)[len(ts) // 2]
+
+
 def kernel_ms(fn_with_events, iters=20):
     L = _abi.lib()
     e0, e1 = C.c_void_p(), C.c_void_p()
@@ -60,8 +86,10 @@ def grpo(name, R, n, dist, streams=("lp", "old_lp", "ref_lp", "mask")):
     bytes_ = T * 17 + b.n_rollouts * 16
     step = lambda: dfx.ppo_loss(b, ctx, adv_source="group", adv_tok_out=True)  # noqa: E731
     ms = timeit(step)
+    gms = graph_ms(step)
     km = kernel_ms(lambda ev: dfx.ppo_loss(b, ctx, adv_source="group", adv_tok_out=True, events=ev))
-    return {"config": name, "tokens": T, "rollouts": b.n_rollouts, "step_ms": ms, "kernel_ms": km,
+    return {"config": name, "tokens": T, "rollouts": b.n_rollouts, "step_ms": ms, "step_graph_ms": gms,
+            "tokens_per_s_graph": T / (gms / 1e3), "kernel_ms": km,
             "tokens_per_s": T / (ms / 1e3), "kernel_gbs": bytes_ / (km / 1e3) / 1e9,
             "kernel_frac_of_hbm": bytes_ / (km / 1e3) / 1e9 / PEAK, "bytes_per_launch": bytes_,
             "step": "fused GRPO group stats + broadcast + clipped surrogate + k3 KL (+adv write)"}
@@ -79,13 +107,13 @@ def ppo_c3():
         dfx.fn_gae_advantage(node, b, ctx)
         dfx.ppo_loss(b, ctx, adv_source="token")
 
-    ms = timeit(step)
-    g_ms = timeit(lambda: dfx.fn_gae_advantage(node, b, ctx))
+    ms = graph_ms(step)
+    g_ms = graph_ms(lambda: dfx.fn_gae_advantage(node, b, ctx))
     km = kernel_ms(lambda ev: dfx.ppo_loss(b, ctx, adv_source="token", events=ev))
     gae_bytes = T * 17
     loss_bytes = T * 17
-    return {"config": "C3", "tokens": T, "step_ms": ms, "tokens_per_s": T / (ms / 1e3),
-            "gae_ms": g_ms, "gae_gbs": gae_bytes / (g_ms / 1e3) / 1e9,
+    return {"config": "C3", "tokens": T, "step_graph_ms": ms, "tokens_per_s": T / (ms / 1e3),
+            "gae_graph_ms": g_ms, "gae_gbs": gae_bytes / (g_ms / 1e3) / 1e9,
             "gae_frac_of_hbm": gae_bytes / (g_ms / 1e3) / 1e9 / PEAK,
             "loss_kernel_ms": km, "loss_gbs": loss_bytes / (km / 1e3) / 1e9,
             "loss_frac_of_hbm": loss_bytes / (km / 1e3) / 1e9 / PEAK,
