@@ -239,3 +239,53 @@ def test_c2_scale_properties(dfx):
     assert np.abs(a.sum(1)).max() < 1e-9
     m = db.streams["mask"][: db.token_span].to(torch.float64).sum().item()
     assert r1[0, 5].item() == m
+
+
+GAE_CASES = [
+    # seed, records, rollouts, dist, min, max, view (records r0, r1 of the batch, or None)
+    (3, 4, 1, "constant", 20000, 20000, None),   # rollouts spanning several 4096-token tiles with no end inside
+    (5, 40, 8, "uniform", 0, 40, None),          # many empty and 1-token rollouts
+    (11, 12, 16, "skewed", 1, 16384, None),      # C5-like skew
+    (9, 16, 4, "uniform", 1, 3000, (3, 11)),     # a view: token_base not 4- or 16-aligned, neighbours untouched
+    (2, 1, 1, "constant", 1, 1, None),           # a single token
+]
+
+
+@pytest.mark.parametrize("case", GAE_CASES)
+def test_gae_shapes(O, dfx, case):
+    """GAE over tile-spanning, empty, skewed and offset (view) rollouts: values within tolerance, whitening
+    count exact, tokens outside the batch untouched."""
+    seed, R, n, kind, lo, hi, view = case
+    sb = make(O, seed, R, n, kind, lo, hi)
+    db = device_batch(dfx, sb)
+    cu = sb.cu_seqlens
+    if view is not None:
+        r0, r1 = view
+        db = db.view_records(r0, r1)
+        s0, s1 = int(sb.group_off[r0]), int(sb.group_off[r1])
+        cu = np.ascontiguousarray(sb.cu_seqlens[s0:s1 + 1])
+    ctx = dfx.StageContext(gae_gamma=0.99, gae_lambda=0.95)
+    b0, b1 = int(cu[0]), int(cu[-1])
+    # through the C ABI with sentinel-filled outputs: tokens outside [b0, b1) must stay untouched
+    from paper_2507_13833_b200 import _abi
+    L = _abi.lib()
+    adv = torch.full_like(db.streams["lp"], 7.0)
+    ret = torch.full_like(db.streams["lp"], 7.0)
+    wsum = torch.zeros(3, dtype=torch.float64, device=adv.device)
+    nb = L.dfx_gae_workspace_bytes(db.n_rollouts, db.token_span)
+    ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=adv.device)
+    st = db.struct()
+    for _ in range(2):  # the workspace is reused: epoch tags and the self-clearing end bitmap
+        _abi.check(L.dfx_gae(C.byref(st), db.token_base, db.token_span, 0.99, 0.95, adv.data_ptr(), ret.data_ptr(),
+                             wsum.data_ptr(), ws.data_ptr(), ws.numel(), None))
+    torch.cuda.synchronize()
+    A, Rt, wref = O.gae(cu, sb.token_reward, sb.value_tok, sb.mask, 0.99, 0.95)
+    got_a, got_r = adv.cpu().numpy(), ret.cpu().numpy()
+    assert_close_vec(got_a[b0:b1], A[b0:b1], "gae adv")
+    assert_close_vec(got_r[b0:b1], Rt[b0:b1], "gae ret")
+    assert (got_a[:b0] == 7.0).all() and (got_a[b1:] == 7.0).all()
+    assert (got_r[:b0] == 7.0).all() and (got_r[b1:] == 7.0).all()
+    wsg = wsum.cpu().numpy()
+    assert wsg[2] == wref[2]
+    if wref[2] > 0:
+        assert_close_vec(wsg[:2], wref[:2], "whiten sums")
