@@ -8,6 +8,9 @@
 //      BufferStore/InprocFabric with one thread per worker: the captured final records equal those of the same
 //      run with builtin_registry(), byte for byte (GRPO 1x4 dp2->dp2/tp2 and PPO 2x2)
 //   4. gpu_train's fused loss on token-stream payloads equals the oracle's f64 loss within 1e-5
+//   5. dfx::DeviceBufferStore (include/dfx_store.hpp) == the reference BufferStore + InprocFabric: for several
+//      (B, W, produced, consumed) layouts, every destination group's batch -- read on every GPU that hosts one of
+//      its TP workers, by one thread per worker -- serializes to the same bytes as the reference get()
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -18,6 +21,7 @@
 #include "distflow/planner.hpp"
 #include "distflow/worker.hpp"
 #include "dfx_distflow.hpp"
+#include "dfx_store.hpp"
 #include "../oracle/dfx_oracle.h"
 
 using namespace distflow;
@@ -269,6 +273,193 @@ static void test_loss() {
   CHECK(versions[Role::ACTOR] == 1, "gpu_train bumps the ACTOR model version");
 }
 
+// ---- 5. device DataBuffer vs the reference BufferStore ---------------------------------------------------------
+static const char* kStreamOrder[5] = {"token_id", "lp", "old_lp", "ref_lp", "mask"};  // payload layout, 17 B/token
+static const size_t kStreamElem[5] = {4, 4, 4, 4, 1};
+
+static std::vector<SampleRecord> store_records(uint32_t G) {
+  std::vector<SampleRecord> recs;
+  for (uint32_t i = 0; i < G; ++i) {
+    SampleRecord r;
+    r.sample_id = 7000 + i;
+    const uint32_t nr = 1 + i % 3;
+    for (uint32_t j = 0; j < nr; ++j) {
+      Rollout ro;
+      ro.token_count = (i * 37 + j * 11) % 50;
+      ro.payload.resize(size_t(ro.token_count) * 17);
+      for (size_t k = 0; k < ro.payload.size(); ++k) ro.payload[k] = uint8_t((i * 131 + j * 17 + k * 7) & 0xff);
+      ro.channels["reward"] = i + 0.25 * j;
+      ro.channels["advantage"] = -double(i) - 0.5 * j;
+      r.rollouts.push_back(ro);
+    }
+    recs.push_back(r);
+  }
+  return recs;
+}
+
+static dfx::DeviceBatch upload_records(int dev, const std::vector<SampleRecord>& recs) {
+  std::vector<uint64_t> ids;
+  std::vector<int32_t> go{0};
+  std::vector<int64_t> cu{0};
+  std::map<std::string, std::vector<double>> ch;
+  std::map<std::string, std::pair<std::vector<uint8_t>, size_t>> st;
+  for (int k = 0; k < 5; ++k) st[kStreamOrder[k]].second = kStreamElem[k];
+  for (const auto& r : recs) {
+    ids.push_back(r.sample_id);
+    for (const auto& ro : r.rollouts) {
+      const size_t L = ro.token_count;
+      size_t off = 0;
+      for (int k = 0; k < 5; ++k) {
+        auto& v = st[kStreamOrder[k]].first;
+        v.insert(v.end(), ro.payload.begin() + off, ro.payload.begin() + off + L * kStreamElem[k]);
+        off += L * kStreamElem[k];
+      }
+      for (const auto& [n, x] : ro.channels) ch[n].push_back(x);
+      cu.push_back(cu.back() + int64_t(L));
+    }
+    go.push_back(int32_t(cu.size() - 1));
+  }
+  return dfx::DeviceBatch::upload(dev, ids, go, cu, ch, st);
+}
+
+static std::vector<SampleRecord> download_records(const dfx::DeviceBatch& b) {
+  auto d2h = [](const void* p, size_t bytes) {
+    std::vector<uint8_t> v(bytes);
+    if (bytes) dfx::store_cuda(cudaMemcpy(v.data(), p, bytes, cudaMemcpyDeviceToHost), "D2H");
+    return v;
+  };
+  const auto ids = d2h(b.ids, size_t(b.n_records) * 8);
+  const auto cu = d2h(b.cu, size_t(b.n_rollouts + 1) * 8);
+  const auto go = d2h(b.group_off, size_t(b.n_records + 1) * 4);
+  std::map<std::string, std::vector<uint8_t>> ch, st;
+  for (const auto& [n, p] : b.channels) ch[n] = d2h(p, size_t(b.n_rollouts) * 8);
+  for (const auto& [n, s] : b.streams) st[n] = d2h(s.base, size_t(b.token_base + b.token_span) * s.elem);
+  std::vector<SampleRecord> out;
+  const int64_t* c = reinterpret_cast<const int64_t*>(cu.data());
+  const int32_t* g = reinterpret_cast<const int32_t*>(go.data());
+  for (int64_t r = 0; r < b.n_records; ++r) {
+    SampleRecord rec;
+    std::memcpy(&rec.sample_id, ids.data() + 8 * r, 8);
+    for (int32_t s = g[r]; s < g[r + 1]; ++s) {
+      Rollout ro;
+      ro.token_count = uint32_t(c[s + 1] - c[s]);
+      for (int k = 0; k < 5; ++k) {
+        const auto& v = st.at(kStreamOrder[k]);
+        ro.payload.insert(ro.payload.end(), v.begin() + c[s] * int64_t(kStreamElem[k]),
+                          v.begin() + c[s + 1] * int64_t(kStreamElem[k]));
+      }
+      for (const auto& [n, v] : ch) {
+        double x;
+        std::memcpy(&x, v.data() + 8 * s, 8);
+        ro.channels[n] = x;
+      }
+      rec.rollouts.push_back(ro);
+    }
+    out.push_back(rec);
+  }
+  return out;
+}
+
+static void test_device_store() {
+  int n_gpu = 0;
+  cudaGetDeviceCount(&n_gpu);
+  struct Cfg {
+    uint32_t B, W, dp_p, tp_p, dp_c, tp_c, G;
+  };
+  const Cfg cfgs[] = {{1, 4, 4, 1, 2, 2, 24}, {1, 8, 8, 1, 4, 2, 64}, {2, 2, 4, 1, 2, 2, 16},
+                      {2, 4, 2, 4, 8, 1, 32}, {2, 4, 8, 1, 2, 4, 48}, {1, 4, 2, 2, 4, 1, 20}};
+  for (const Cfg& c : cfgs) {
+    const auto recs = store_records(c.G);
+    const ClusterTopology topo{c.B, c.W};
+    const ParallelLayout produced{c.dp_p, c.tp_p}, consumed{c.dp_c, c.tp_c};
+    // the reference: B stores over one InprocFabric
+    InprocFabric fabric(topo);
+    std::map<std::string, StoreStagePlan> stages;
+    stages["s"] = StoreStagePlan{produced, consumed, tags::kRedistBase};
+    std::vector<std::unique_ptr<BufferStore>> stores;
+    std::vector<BufferStore*> ptrs;
+    for (uint32_t b = 0; b < c.B; ++b) {
+      stores.push_back(std::make_unique<BufferStore>(topo, b, &fabric, stages));
+      ptrs.push_back(stores.back().get());
+    }
+    // the device store: logical worker w on GPU w * n_gpu / (B W)
+    const uint32_t world = c.B * c.W;
+    std::vector<int> gpu(world);
+    for (uint32_t w = 0; w < world; ++w) gpu[w] = int(uint64_t(w) * uint64_t(n_gpu) / world);
+    std::map<std::string, dfx::StagePlan> dstages;
+    dstages["s"] = dfx::StagePlan{{c.dp_p, c.tp_p}, true, {c.dp_c, c.tp_c}};
+    dfx::DeviceBufferStore dstore(c.B, c.W, gpu, dstages);
+    const uint32_t per = c.G / c.dp_p;
+    for (uint32_t p = 0; p < c.dp_p; ++p) {
+      SampleBatch batch;
+      batch.stage_id = "s";
+      batch.records.assign(recs.begin() + p * per, recs.begin() + (p + 1) * per);
+      const uint32_t lead = produced.group_lead(p);
+      const dfx::DeviceBatch db = upload_records(gpu[lead], batch.records);
+      for (uint32_t t = 0; t < c.tp_p; ++t) {
+        stores[topo.node_of(lead)]->put("s", 0, p, t, batch);
+        dstore.put("s", 0, p, t, db);
+      }
+    }
+    redistribute(ptrs, "s", 0, consumed);
+    // one thread per logical worker reads its consumer group on its GPU (SPMD, like run_iteration)
+    std::vector<std::vector<uint8_t>> got(world);
+    std::vector<std::string> errs(world);
+    std::vector<std::thread> th;
+    for (uint32_t w = 0; w < world; ++w)
+      th.emplace_back([&, w] {
+        try {
+          cudaSetDevice(gpu[w]);
+          const dfx::DeviceBatch b = dstore.get("s", 0, consumed.dp_rank(w), dfx::Layout{c.dp_c, c.tp_c});
+          got[w] = serialize_records(download_records(b));
+          dstore.worker_done(0);
+        } catch (const std::exception& e) {
+          errs[w] = e.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    bool ok = true;
+    for (uint32_t w = 0; w < world; ++w) {
+      if (!errs[w].empty()) {
+        std::printf("  worker %u: %s\n", w, errs[w].c_str());
+        ok = false;
+        continue;
+      }
+      const uint32_t d = consumed.dp_rank(w);
+      const SampleBatch want = stores[topo.node_of(consumed.group_lead(d))]->get("s", 0, d, consumed);
+      ok = ok && got[w] == serialize_records(want.records);
+    }
+    ok = ok && dstore.suppressed_count() == uint64_t(c.dp_p) * (c.tp_p - 1);
+    char name[160];
+    std::snprintf(name, sizeof(name), "device store == reference BufferStore (B%u W%u dp%u tp%u -> dp%u tp%u, %d GPU)",
+                  c.B, c.W, c.dp_p, c.tp_p, c.dp_c, c.tp_c, n_gpu);
+    CHECK(ok, name);
+  }
+  // semantics: stale puts / gets and NotReadyError, as the reference
+  std::map<std::string, dfx::StagePlan> st1;
+  st1["s"] = dfx::StagePlan{{2, 1}, true, {1, 2}};
+  dfx::DeviceBufferStore s1(1, 2, {0, 0}, st1);
+  bool not_ready = false, stale = false, unknown = false;
+  try {
+    s1.ensure_ready("s", 0, dfx::Layout{1, 2}, std::chrono::milliseconds(20));
+  } catch (const dfx::StoreError& e) {
+    not_ready = e.code == DFX_NOT_READY;
+  }
+  s1.worker_done(0);
+  s1.worker_done(0);
+  try {
+    s1.put("s", 0, 0, 0, upload_records(0, store_records(2)));
+  } catch (const dfx::StoreError& e) {
+    stale = e.code == DFX_STALE_ITERATION;
+  }
+  try {
+    s1.put("nope", 1, 0, 0, upload_records(0, store_records(2)));
+  } catch (const dfx::StoreError& e) {
+    unknown = e.code == DFX_UNKNOWN_STAGE;
+  }
+  CHECK(not_ready && stale && unknown, "device store errors: NotReady / StaleIteration / UnknownStage");
+}
+
 int main() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -279,6 +470,7 @@ int main() {
   test_errors();
   test_chain();
   test_loss();
+  test_device_store();
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
 }
