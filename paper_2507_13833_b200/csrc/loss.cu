@@ -474,7 +474,6 @@ __global__ void __launch_bounds__(256) mask_count_kernel(MaskCountParams mp, int
 // reduces the block partials in index order. COUNTS: the dlogp pre-pass.
 // ---------------------------------------------------------------------------
 constexpr int kFinThreads = 256;
-constexpr int kFinSeqPerThread = 1;
 
 struct FinParams {
   int n_src;
@@ -523,11 +522,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
   const int64_t sr0 = f.lgo ? f.lgo[gi] : 0;
   const int64_t sr1 = f.lgo ? f.lgo[gi + 1] : f.n_roll;
   double acc[6] = {0, 0, 0, 0, 0, 0};  // pg, kl, clip, akl, n, S
-  const int64_t first = sr0 + (int64_t)blockIdx.x * kFinThreads * kFinSeqPerThread;
-#pragma unroll
-  for (int j = 0; j < kFinSeqPerThread; ++j) {
-    const int64_t s = first + (int64_t)j * kFinThreads + threadIdx.x;
-    if (s >= sr1) break;
+  // block b of a group sums rollouts [first, last) with a thread stride (fixed order: deterministic)
+  const int64_t per = (sr1 - sr0 + f.nb - 1) / f.nb;
+  const int64_t first = sr0 + (int64_t)blockIdx.x * per, last = min(sr1, first + per);
+  for (int64_t s = first + threadIdx.x; s < last; s += kFinThreads) {
     const LossSrc& S = f.src[src_of_roll(f.src, f.n_src, s)];
     const int64_t sl = s - S.roll0;
     const int64_t a = S.g.cu[sl], b = S.g.cu[sl + 1];
@@ -559,23 +557,28 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
     }
   }
   block_sum<6>(acc, sh);
-  double* blk = f.blk + ((int64_t)gi * f.nb + blockIdx.x) * 6;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < 6; ++q) blk[q] = acc[q];
-    __threadfence();
-    const unsigned t = atomicAdd(f.ticket + gi, 1u);
-    is_last = (t == (unsigned)f.nb - 1);
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
   double tot[6] = {0, 0, 0, 0, 0, 0};
-  const volatile double* vb = f.blk + (int64_t)gi * f.nb * 6;
-  for (int i = threadIdx.x; i < f.nb; i += kFinThreads)
+  if (f.nb == 1) {  // one block per group (small batches): no second phase
 #pragma unroll
-    for (int q = 0; q < 6; ++q) tot[q] += vb[(int64_t)i * 6 + q];
-  block_sum<6>(tot, sh);
+    for (int q = 0; q < 6; ++q) tot[q] = acc[q];
+  } else {
+    double* blk = f.blk + ((int64_t)gi * f.nb + blockIdx.x) * 6;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) blk[q] = acc[q];
+      __threadfence();
+      const unsigned t = atomicAdd(f.ticket + gi, 1u);
+      is_last = (t == (unsigned)f.nb - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const volatile double* vb = f.blk + (int64_t)gi * f.nb * 6;
+    for (int i = threadIdx.x; i < f.nb; i += kFinThreads)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) tot[q] += vb[(int64_t)i * 6 + q];
+    block_sum<6>(tot, sh);
+  }
   if (threadIdx.x == 0) {
     const double N = tot[4], S = tot[5];
     if (COUNTS) {
@@ -620,7 +623,8 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t n_slots, int32_t n_groups) {
   LossWs w{};
-  w.nb = (int)std::max<int64_t>(1, (n_seq + kFinThreads * kFinSeqPerThread - 1) / (kFinThreads * kFinSeqPerThread));
+  // finalize blocks per loss group: one block (no inter-block phase) up to 4096 rollouts, else 256 per block
+  w.nb = n_seq <= 4096 ? 1 : (int)((n_seq + kFinThreads - 1) / kFinThreads);
   size_t off = 0;
   char* b = static_cast<char*>(base);
   auto take = [&](size_t bytes) {

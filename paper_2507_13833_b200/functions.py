@@ -190,7 +190,7 @@ def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
     like = batch.streams["token_reward"]
     adv = torch.empty_like(like)  # every token of the span is written
     ret = torch.empty_like(like)
-    wsum = torch.zeros(3, dtype=torch.float64, device=batch.device)
+    wsum = torch.empty(3, dtype=torch.float64, device=batch.device)  # written by the call (memset if empty)
     nbytes = _abi.lib().dfx_gae_workspace_bytes(batch.n_rollouts, batch.token_span)
     ws = ctx.workspace.get("gae", nbytes, batch.device)
     st = batch.struct()
