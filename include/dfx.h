@@ -269,6 +269,30 @@ dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs, int32_t n_segs, int32_t 
                               int32_t* dst_group_off, int32_t* dst_roll_group, int64_t* dst_cu,
                               double* const* dst_ch, dfx_stream stream);
 
+/* ---------------------------------------------------------------------------
+ * The reference's record wire format on the device:
+ * serialize_records (distflow/record.hpp:109-127, 151-156) of a packed batch,
+ * byte-identical to the CPU serializer, so device batches can be handed to CPU
+ * peers (Fabric / BufferStore::exchange) without a host repack.
+ * Payload of rollout s: for each stream k in order, its tokens' elements
+ * (esz[k] bytes each) -- e.g. token_id i32 | lp f32 | old f32 | ref f32 | mask u8.
+ * Channels in the given order (pass them sorted by name: std::map order).
+ * meta_blob/meta_off (device, nullable): each record's pre-serialized meta
+ * section (u32 count + (str, str)*); NULL writes an empty section.
+ * tok_count (device, nullable): Rollout::token_count, default cu[s+1]-cu[s].
+ * dfx_serialize_plan (host-only) fills rec_off[n_records+1] (byte offset of
+ * each record after the leading u32) from host copies of group_off / cu /
+ * meta_off and returns the blob size, or -status. Copy rec_off to the device
+ * for dfx_serialize_records. meta_blob must be readable 4 bytes past its end.
+ * ------------------------------------------------------------------------- */
+int64_t dfx_serialize_plan(int64_t n_records, const int32_t* h_group_off, const int64_t* h_cu,
+                           const int64_t* h_meta_off, int32_t n_streams, const uint32_t* esz, int32_t n_ch,
+                           const char* const* ch_names, int64_t* rec_off);
+dfx_status dfx_serialize_records(const dfx_packed* b, const uint64_t* ids, const uint32_t* tok_count,
+                                 int32_t n_streams, const void* const* streams, const uint32_t* esz, int32_t n_ch,
+                                 const char* const* ch_names, const double* const* ch, const uint8_t* meta_blob,
+                                 const int64_t* meta_off, const int64_t* rec_off, uint8_t* out, dfx_stream stream);
+
 /* Peer memory for the NVLink pull transport. dfx_ipc_export returns the IPC
  * handle of the allocation containing ptr and ptr's offset in it; a peer maps
  * it with dfx_ipc_open. Map a peer process's allocation

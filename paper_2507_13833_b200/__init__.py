@@ -14,5 +14,6 @@ from .functions import (FunctionRegistry, LossConfig, NodeSpec, StageContext, bu
                         ppo_loss, ppo_loss_sources, preset_dag, registry_bind)
 from .packed import PackedBatch  # noqa: E402,F401
 from .synth import TokenDist  # noqa: E402,F401
+from . import wire  # noqa: E402,F401
 
 __version__ = "0.1.0"

@@ -1,0 +1,209 @@
+// blob.cu -- the reference's record wire format on the device.
+//
+// serialize_records (distflow/record.hpp:109-127, 151-156) of a packed batch, written by the GPU straight from the
+// SoA token streams into the little-endian blob that CPU peers (Fabric, BufferStore::exchange) read:
+//   u32 n_records; per record: u64 sample_id | meta section (u32 count + (str, str)*) | u32 n_rollouts;
+//   per rollout: u32 token_count | u64 payload_len | payload | u32 n_channels | (u32 len, name, f64 bits)*
+// The payload of rollout s is the concatenation, stream by stream, of its tokens' elements (token_id
+// i32 | lp f32 | old f32 | ref f32 | mask u8). Record offsets come from a host plan (dfx_serialize_plan: every size
+// is known from the host copies of group_off / cu), so every rollout finds its offset in O(1) and one CTA per
+// rollout writes its header, payload and channels in parallel. Payload bytes land at arbitrary byte offsets: the
+// interior is written as aligned 32-bit words assembled with funnel shifts from aligned source words, the
+// (at most two) partial words at either end byte by byte, so neighbouring writers never share a store.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dfx {
+
+constexpr int kBlobMaxStreams = 8;
+constexpr int kBlobMaxCh = 8;
+constexpr int kBlobMaxName = 48;
+
+struct BlobParams {
+  int64_t n_records, n_rollouts;
+  const uint64_t* ids;
+  const int32_t* group_off;
+  const int64_t* cu;
+  const uint32_t* tok_count;  // nullable: cu[s+1] - cu[s]
+  int n_streams;
+  const uint8_t* streams[kBlobMaxStreams];
+  uint32_t esz[kBlobMaxStreams];
+  uint32_t E;                 // sum of esz
+  int n_ch;
+  const double* ch[kBlobMaxCh];
+  uint32_t name_len[kBlobMaxCh];
+  char names[kBlobMaxCh][kBlobMaxName];
+  uint32_t CH;                // bytes of one rollout's channel entries
+  const uint8_t* meta;        // nullable: per-record pre-serialized meta sections
+  const int64_t* meta_off;
+  const int64_t* rec_off;     // [n_records + 1] blob offset of each record (after the leading u32)
+  uint8_t* out;
+};
+
+__device__ __forceinline__ void put_le(uint8_t* p, uint64_t v, int n) {
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) p[i] = uint8_t(v >> (8 * i));
+}
+
+// Copy n bytes src -> dst (any alignment) with the block's threads: interior as aligned u32 stores built from two
+// aligned u32 loads and a funnel shift, the partial words at either end byte by byte.
+__device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+  if (n == 0) return;
+  const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst), d1 = d0 + n;
+  const uintptr_t a0 = (d0 + 3) & ~uintptr_t(3), a1 = d1 & ~uintptr_t(3);
+  if (a1 <= a0) {  // shorter than one aligned word
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    return;
+  }
+  const uint64_t head = a0 - d0, tail = d1 - a1;
+  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+  if (threadIdx.x < tail) dst[n - tail + threadIdx.x] = src[n - tail + threadIdx.x];
+  // word w of the interior covers source bytes [head + 4w, head + 4w + 4)
+  const uint8_t* s = src + head;
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(s);
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(sa & 3u) * 8u;
+  uint32_t* dw = reinterpret_cast<uint32_t*>(a0);
+  const uint64_t nw = (a1 - a0) / 4;
+  if (sh == 0) {
+    for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x) dw[w] = __ldg(sw + w);
+  } else {
+    for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x) dw[w] = __funnelshift_r(__ldg(sw + w), __ldg(sw + w + 1), sh);
+  }
+}
+
+__global__ void __launch_bounds__(256) serialize_kernel(BlobParams p) {
+  const int64_t b = blockIdx.x;
+  if (b == 0 && threadIdx.x == 0) put_le(p.out, uint64_t(p.n_records), 4);
+  // record header of record b (every record, including ones without rollouts)
+  if (b < p.n_records) {
+    uint8_t* o = p.out + 4 + p.rec_off[b];
+    const int32_t g0 = p.group_off[b], g1 = p.group_off[b + 1];
+    int64_t mlen = 4;
+    if (p.meta) {
+      mlen = p.meta_off[b + 1] - p.meta_off[b];
+      block_copy(o + 8, p.meta + p.meta_off[b], uint64_t(mlen));
+    }
+    if (threadIdx.x == 0) {
+      put_le(o, p.ids[b], 8);
+      if (!p.meta) put_le(o + 8, 0, 4);
+      put_le(o + 8 + mlen, uint64_t(g1 - g0), 4);
+    }
+  }
+  if (b >= p.n_rollouts) return;
+  // rollout b: its record by a binary search over group_off, then its offset in O(1)
+  __shared__ int64_t s_rec;
+  if (threadIdx.x == 0) {
+    int64_t lo = 0, hi = p.n_records;  // last record with group_off[r] <= b
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (p.group_off[mid] <= b) lo = mid;
+      else hi = mid;
+    }
+    while (lo + 1 < p.n_records && p.group_off[lo + 1] <= b) ++lo;  // skip empty records
+    s_rec = lo;
+  }
+  __syncthreads();
+  const int64_t r = s_rec;
+  const int32_t g0 = p.group_off[r];
+  const int64_t mlen = p.meta ? p.meta_off[r + 1] - p.meta_off[r] : 4;
+  const int64_t t0 = p.cu[b], t1 = p.cu[b + 1], L = t1 - t0;
+  // record header: u64 id + meta section + u32 n_rollouts = 12 + mlen; each rollout: 16 + payload + channels
+  const uint64_t off = uint64_t(p.rec_off[r]) + 12 + uint64_t(mlen) + uint64_t(b - g0) * (16u + p.CH) +
+                       uint64_t(t0 - p.cu[g0]) * p.E;
+  uint8_t* o = p.out + 4 + off;
+  const uint64_t plen = uint64_t(L) * p.E;
+  if (threadIdx.x == 0) {
+    put_le(o, p.tok_count ? p.tok_count[b] : uint32_t(L), 4);
+    put_le(o + 4, plen, 8);
+  }
+  uint64_t po = 12;
+  for (int k = 0; k < p.n_streams; ++k) {
+    block_copy(o + po, p.streams[k] + uint64_t(t0) * p.esz[k], uint64_t(L) * p.esz[k]);
+    po += uint64_t(L) * p.esz[k];
+  }
+  uint8_t* c = o + 12 + plen;
+  if (threadIdx.x == 0) put_le(c, uint64_t(p.n_ch), 4);
+  uint64_t co = 4;
+  for (int k = 0; k < p.n_ch; ++k) {
+    const uint32_t nl = p.name_len[k];
+    if (threadIdx.x == 0) put_le(c + co, nl, 4);
+    for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) c[co + 4 + i] = uint8_t(p.names[k][i]);
+    if (threadIdx.x == 0) put_le(c + co + 4 + nl, uint64_t(__double_as_longlong(p.ch[k][b])), 8);
+    co += 12 + nl;
+  }
+}
+
+}  // namespace dfx
+
+using namespace dfx;
+
+extern "C" {
+
+int64_t dfx_serialize_plan(int64_t n_records, const int32_t* h_group_off, const int64_t* h_cu,
+                           const int64_t* h_meta_off, int32_t n_streams, const uint32_t* esz, int32_t n_ch,
+                           const char* const* ch_names, int64_t* rec_off) {
+  if (n_records < 0 || !h_group_off || (n_records > 0 && !h_cu) || !rec_off) {
+    set_error("dfx_serialize_plan: bad argument");
+    return -DFX_INVALID_ARGUMENT;
+  }
+  uint64_t E = 0, CH = 0;
+  for (int32_t k = 0; k < n_streams; ++k) E += esz[k];
+  for (int32_t c = 0; c < n_ch; ++c) CH += 12 + std::strlen(ch_names[c]);
+  int64_t o = 0;
+  for (int64_t r = 0; r < n_records; ++r) {
+    rec_off[r] = o;
+    const int32_t g0 = h_group_off[r], g1 = h_group_off[r + 1];
+    const int64_t meta = h_meta_off ? h_meta_off[r + 1] - h_meta_off[r] : 4;
+    o += 12 + meta + int64_t(g1 - g0) * int64_t(16 + CH) + (h_cu[g1] - h_cu[g0]) * int64_t(E);
+  }
+  rec_off[n_records] = o;
+  return 4 + o;  // leading u32 record count
+}
+
+dfx_status dfx_serialize_records(const dfx_packed* b, const uint64_t* ids, const uint32_t* tok_count, int32_t n_streams,
+                                 const void* const* streams, const uint32_t* esz, int32_t n_ch,
+                                 const char* const* ch_names, const double* const* ch, const uint8_t* meta_blob,
+                                 const int64_t* meta_off, const int64_t* rec_off, uint8_t* out, dfx_stream stream) {
+  if (!b || !ids || !out || !rec_off || n_streams < 0 || n_streams > kBlobMaxStreams || n_ch < 0 || n_ch > kBlobMaxCh ||
+      (n_streams && (!streams || !esz)) || (n_ch && (!ch_names || !ch)) || (meta_blob && !meta_off))
+    return fail(DFX_INVALID_ARGUMENT, "dfx_serialize_records: bad argument");
+  if (b->n_records > 0 && (!b->group_off || !b->cu_seqlens))
+    return fail(DFX_INVALID_ARGUMENT, "dfx_serialize_records: packed batch lacks group_off/cu_seqlens");
+  BlobParams p{};
+  p.n_records = b->n_records;
+  p.n_rollouts = b->n_rollouts;
+  p.ids = ids;
+  p.group_off = b->group_off;
+  p.cu = b->cu_seqlens;
+  p.tok_count = tok_count;
+  p.n_streams = n_streams;
+  for (int k = 0; k < n_streams; ++k) {
+    p.streams[k] = static_cast<const uint8_t*>(streams[k]);
+    p.esz[k] = esz[k];
+    p.E += esz[k];
+  }
+  p.n_ch = n_ch;
+  for (int k = 0; k < n_ch; ++k) {
+    const size_t nl = std::strlen(ch_names[k]);
+    if (nl >= size_t(kBlobMaxName)) return fail(DFX_INVALID_ARGUMENT, "dfx_serialize_records: channel name too long");
+    std::memcpy(p.names[k], ch_names[k], nl);
+    p.name_len[k] = uint32_t(nl);
+    p.ch[k] = ch[k];
+    p.CH += 12 + uint32_t(nl);
+  }
+  p.meta = meta_blob;
+  p.meta_off = meta_off;
+  p.rec_off = rec_off;
+  p.out = out;
+  const int64_t grid = std::max<int64_t>(std::max<int64_t>(p.n_records, p.n_rollouts), 1);
+  serialize_kernel<<<(unsigned)grid, 256, 0, stream>>>(p);
+  DFX_LAUNCH_CHECK("serialize_kernel");
+  return DFX_OK;
+}
+
+}  // extern "C"

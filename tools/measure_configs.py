@@ -154,6 +154,19 @@ def reshard_c4():
             "placements": res}
 
 
+def wire_c4():
+    """Device serialize_records of a C4-size batch (16.8M tokens, 17 B/token payload + reward/advantage)."""
+    from paper_2507_13833_b200 import wire
+    b = dfx.PackedBatch.synthetic(11, 1024, 16, dfx.TokenDist("constant", 1024),
+                                  streams=("token_id", "lp", "old_lp", "ref_lp", "mask"))
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), b, dfx.StageContext())
+    out = wire.serialize(b, channels=("advantage", "reward"))
+    n = out.numel()
+    ms = timeit(lambda: wire.serialize(b, channels=("advantage", "reward")), iters=10, warm=2)
+    return {"config": "C4 wire (device serialize_records)", "tokens": b.token_span, "blob_bytes": n, "ms": ms,
+            "gbs_rw": 2 * n / (ms / 1e3) / 1e9, "frac_of_hbm": 2 * n / (ms / 1e3) / 1e9 / PEAK}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -162,7 +175,8 @@ def main():
             grpo("C2", 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096)),
             ppo_c3(),
             grpo("C5/8 (one GPU's share: 512 prompts)", 512, 16, dfx.TokenDist("skewed", 0, 1, 16384)),
-            reshard_c4()]
+            reshard_c4(),
+            wire_c4()]
     for r in rows:
         print(json.dumps(r), flush=True)
     if a.out:
