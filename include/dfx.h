@@ -293,6 +293,23 @@ dfx_status dfx_serialize_records(const dfx_packed* b, const uint64_t* ids, const
                                  const char* const* ch_names, const double* const* ch, const uint8_t* meta_blob,
                                  const int64_t* meta_off, const int64_t* rec_off, uint8_t* out, dfx_stream stream);
 
+/* deserialize_records (record.hpp:129-149, 158-165) into a packed batch: a
+ * host header walk builds the index (call once with every output NULL for
+ * the counts, then with arrays: ids[R], meta_range[2R] (start, end of record
+ * r's meta section in the blob), group_off[R+1], cu[S+1], tok_count[S], payload_off[S], ch_off[S]);
+ * every rollout must carry the channels ch_names (blob order) and a payload of
+ * a whole number of bytes_per_token. A truncated or malformed blob returns
+ * DFX_ERROR (the reference's ParseError). dfx_blob_unpack then gathers, on the
+ * device, every payload into the token streams and the channel values into
+ * f64 arrays (blob, cu, payload_off, ch_off: device copies). */
+dfx_status dfx_blob_index(const uint8_t* blob, uint64_t size, uint32_t bytes_per_token, int32_t n_ch,
+                          const char* const* ch_names, int64_t* n_records, int64_t* n_rollouts, int64_t* n_tokens,
+                          uint64_t* ids, int64_t* meta_range, int32_t* group_off, int64_t* cu, uint32_t* tok_count,
+                          int64_t* payload_off, int64_t* ch_off);
+dfx_status dfx_blob_unpack(const uint8_t* blob, int64_t n_rollouts, const int64_t* cu, const int64_t* payload_off,
+                           const int64_t* ch_off, int32_t n_streams, void* const* streams, const uint32_t* esz,
+                           int32_t n_ch, const char* const* ch_names, double* const* ch, dfx_stream stream);
+
 /* Peer memory for the NVLink pull transport. dfx_ipc_export returns the IPC
  * handle of the allocation containing ptr and ptr's offset in it; a peer maps
  * it with dfx_ipc_open. Map a peer process's allocation

@@ -207,3 +207,176 @@ dfx_status dfx_serialize_records(const dfx_packed* b, const uint64_t* ids, const
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------------------------
+// deserialize_records (record.hpp:129-149, 158-165) into a packed batch: the CPU walks the headers (an index of
+// record ids, rollout token counts and the byte offsets of every payload and channel block -- a sequential parse,
+// microseconds per thousand rollouts), the GPU gathers the payload bytes into the SoA token streams and the f64
+// channels (one CTA per rollout, unaligned source reads assembled with funnel shifts).
+// ---------------------------------------------------------------------------------------------------------------
+namespace dfx {
+
+struct UnblobParams {
+  int64_t n_rollouts;
+  const uint8_t* blob;
+  const int64_t* payload_off;  // [S]
+  const int64_t* ch_off;       // [S] offset of the f64 of channel 0 entry block (after u32 n_channels)
+  const int64_t* cu;           // [S+1] destination token offsets
+  int n_streams;
+  uint8_t* streams[kBlobMaxStreams];
+  uint32_t esz[kBlobMaxStreams];
+  int n_ch;
+  uint32_t ch_val_off[kBlobMaxCh];  // byte offset of channel c's f64 within the channel block
+  double* ch[kBlobMaxCh];
+};
+
+// dst aligned to 4 bytes at its start (element streams are), src any alignment
+__device__ __forceinline__ void block_gather(uint8_t* dst, const uint8_t* src, uint64_t n) {
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(sa & 3u) * 8u;
+  const uint64_t nw = n / 4;
+  uint32_t* dw = reinterpret_cast<uint32_t*>(dst);
+  if (reinterpret_cast<uintptr_t>(dst) & 3u) {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    return;
+  }
+  for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x)
+    dw[w] = sh ? __funnelshift_r(__ldg(sw + w), __ldg(sw + w + 1), sh) : __ldg(sw + w);
+  for (uint64_t i = nw * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(256) unblob_kernel(UnblobParams p) {
+  const int64_t s = blockIdx.x;
+  if (s >= p.n_rollouts) return;
+  const int64_t t0 = p.cu[s], L = p.cu[s + 1] - t0;
+  const uint8_t* src = p.blob + p.payload_off[s];
+  for (int k = 0; k < p.n_streams; ++k) {
+    block_gather(p.streams[k] + uint64_t(t0) * p.esz[k], src, uint64_t(L) * p.esz[k]);
+    src += uint64_t(L) * p.esz[k];
+  }
+  if (threadIdx.x < p.n_ch) {
+    const uint8_t* v = p.blob + p.ch_off[s] + p.ch_val_off[threadIdx.x];
+    uint64_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bits |= uint64_t(v[i]) << (8 * i);
+    p.ch[threadIdx.x][s] = __longlong_as_double((long long)bits);
+  }
+}
+
+}  // namespace dfx
+
+extern "C" {
+
+// Host-side header walk of a record blob. First call with every output NULL returns counts in *n_records /
+// *n_rollouts / *n_tokens (and checks the format); the second fills the arrays. Every rollout must carry the
+// channels ch_names (in blob order, i.e. sorted) and a payload of token_count * bytes_per_token bytes.
+dfx_status dfx_blob_index(const uint8_t* blob, uint64_t size, uint32_t bytes_per_token, int32_t n_ch,
+                          const char* const* ch_names, int64_t* n_records, int64_t* n_rollouts, int64_t* n_tokens,
+                          uint64_t* ids, int64_t* meta_range, int32_t* group_off, int64_t* cu, uint32_t* tok_count,
+                          int64_t* payload_off, int64_t* ch_off) {
+  if (!blob || !n_records || !n_rollouts || !n_tokens) return fail(DFX_INVALID_ARGUMENT, "dfx_blob_index: null argument");
+  uint64_t pos = 0;
+  auto need = [&](uint64_t n) {
+    if (pos + n > size) throw std::string("record blob truncated");  // blob::Reader::need (record.hpp:99-101)
+  };
+  auto u32 = [&]() {
+    need(4);
+    uint32_t v = uint32_t(blob[pos]) | uint32_t(blob[pos + 1]) << 8 | uint32_t(blob[pos + 2]) << 16 |
+                 uint32_t(blob[pos + 3]) << 24;
+    pos += 4;
+    return v;
+  };
+  auto u64 = [&]() {
+    const uint64_t lo = u32();
+    return lo | uint64_t(u32()) << 32;
+  };
+  try {
+    const uint32_t R = u32();
+    int64_t S = 0, T = 0;
+    if (group_off) group_off[0] = 0;
+    if (cu) cu[0] = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      const uint64_t id = u64();
+      if (ids) ids[r] = id;
+      if (meta_range) meta_range[2 * r] = int64_t(pos);
+      const uint32_t nmeta = u32();
+      for (uint32_t m = 0; m < 2 * nmeta; ++m) {
+        const uint32_t n = u32();
+        need(n);
+        pos += n;
+      }
+      if (meta_range) meta_range[2 * r + 1] = int64_t(pos);
+      const uint32_t nroll = u32();
+      for (uint32_t j = 0; j < nroll; ++j, ++S) {
+        const uint32_t tc = u32();
+        const uint64_t plen = u64();
+        if (bytes_per_token == 0 || plen % bytes_per_token)
+          throw std::string("payload of rollout " + std::to_string(S) + " is not a whole number of tokens");
+        const int64_t L = int64_t(plen / bytes_per_token);
+        need(plen);
+        if (payload_off) payload_off[S] = int64_t(pos);
+        if (tok_count) tok_count[S] = tc;
+        pos += plen;
+        T += L;
+        if (cu) cu[S + 1] = T;
+        const uint32_t nch = u32();
+        if (int32_t(nch) != n_ch) throw std::string("rollout " + std::to_string(S) + " has a different channel set");
+        if (ch_off) ch_off[S] = int64_t(pos);
+        for (uint32_t c = 0; c < nch; ++c) {
+          const uint32_t nl = u32();
+          need(nl);
+          if (ch_names && (std::strlen(ch_names[c]) != nl || std::memcmp(blob + pos, ch_names[c], nl) != 0))
+            throw std::string("rollout " + std::to_string(S) + " channel " + std::to_string(c) + " is not '" +
+                              ch_names[c] + "'");
+          pos += nl;
+          need(8);
+          pos += 8;
+        }
+      }
+      if (group_off) group_off[r + 1] = int32_t(S);
+    }
+    if (pos != size) throw std::string("trailing bytes after the last record");
+    *n_records = R;
+    *n_rollouts = S;
+    *n_tokens = T;
+  } catch (const std::string& e) {
+    return fail(DFX_ERROR, "dfx_blob_index: " + e);  // distflow::ParseError
+  }
+  return DFX_OK;
+}
+
+// Gather payloads and channels of an indexed blob (device copy of the blob, device copies of the index arrays)
+// into the token streams (element k of rollout s at streams[k] + (cu[s] + i) * esz[k]) and f64 channels.
+dfx_status dfx_blob_unpack(const uint8_t* blob, int64_t n_rollouts, const int64_t* cu, const int64_t* payload_off,
+                           const int64_t* ch_off, int32_t n_streams, void* const* streams, const uint32_t* esz,
+                           int32_t n_ch, const char* const* ch_names, double* const* ch, dfx_stream stream) {
+  if (n_rollouts <= 0) return DFX_OK;
+  if (!blob || !cu || !payload_off || n_streams < 0 || n_streams > kBlobMaxStreams || n_ch < 0 || n_ch > kBlobMaxCh ||
+      (n_ch && (!ch_off || !ch || !ch_names)))
+    return fail(DFX_INVALID_ARGUMENT, "dfx_blob_unpack: bad argument");
+  UnblobParams p{};
+  p.n_rollouts = n_rollouts;
+  p.blob = blob;
+  p.payload_off = payload_off;
+  p.ch_off = ch_off;
+  p.cu = cu;
+  p.n_streams = n_streams;
+  for (int k = 0; k < n_streams; ++k) {
+    p.streams[k] = static_cast<uint8_t*>(streams[k]);
+    p.esz[k] = esz[k];
+  }
+  p.n_ch = n_ch;
+  uint32_t o = 0;
+  for (int c = 0; c < n_ch; ++c) {
+    const uint32_t nl = uint32_t(std::strlen(ch_names[c]));
+    p.ch_val_off[c] = o + 4 + nl;
+    p.ch[c] = ch[c];
+    o += 12 + nl;
+  }
+  unblob_kernel<<<(unsigned)n_rollouts, 256, 0, stream>>>(p);
+  DFX_LAUNCH_CHECK("unblob_kernel");
+  return DFX_OK;
+}
+
+}  // extern "C"

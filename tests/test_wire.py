@@ -103,3 +103,40 @@ def test_device_blob_matches_reference(O, dfx, seed, R, n, lo, hi, meta, view):
         ref = O.serialize_packed(ids, go, tc, cu, [getattr(sb, k)[:T] for k in STREAMS], {"reward": rew, "value": val},
                                  meta_off=mo, meta_blob=mb, use_reference=True)
         assert want.tobytes() == ref.tobytes()
+
+
+def test_blob_index_rejects_malformed(O, dfx):
+    """Header walk on the CPU: truncation and channel-set mismatches raise (the reference's ParseError)."""
+    from paper_2507_13833_b200 import errors, wire
+    sb = _host(O, 7, 6, 2, 1, 20)
+    T = sb.n_tokens
+    blob = O.serialize_packed(sb.ids, sb.group_off, sb.tok_count, sb.cu_seqlens, [getattr(sb, k)[:T] for k in STREAMS],
+                              {"advantage": sb.reward, "reward": sb.reward})
+    with pytest.raises(errors.Error):
+        wire.deserialize(blob[:-3], device="cpu")
+    with pytest.raises(errors.Error):
+        wire.deserialize(blob, channels=("reward",), device="cpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,R,n,lo,hi,meta", [(3, 33, 5, 0, 37, True), (7, 16, 2, 16, 48, False)])
+def test_blob_round_trip(O, dfx, seed, R, n, lo, hi, meta):
+    """reference bytes -> device batch (dfx_blob_index + dfx_blob_unpack) -> device bytes: identical, and the
+    device streams / channels equal the records' values bit for bit."""
+    from paper_2507_13833_b200 import wire
+    sb = _host(O, seed, R, n, lo, hi)
+    T = sb.n_tokens
+    mb, mo = _meta(R, seed) if meta else (None, None)
+    blob = O.serialize_packed(sb.ids, sb.group_off, sb.tok_count, sb.cu_seqlens, [getattr(sb, k)[:T] for k in STREAMS],
+                              {"advantage": sb.value, "reward": sb.reward}, meta_off=mo, meta_blob=mb)
+    b, (meta_blob, meta_off, tc) = wire.deserialize(blob)
+    assert tc.tolist() == sb.tok_count.tolist()
+    for k in STREAMS:
+        assert b.streams[k][:T].cpu().numpy().tobytes() == getattr(sb, k)[:T].tobytes(), k
+    assert b.channels["reward"].cpu().numpy().tobytes() == sb.reward.tobytes()
+    assert b.channels["advantage"].cpu().numpy().tobytes() == sb.value.tobytes()
+    if meta:
+        assert meta_blob.tobytes() == mb.tobytes() and meta_off.tolist() == mo.tolist()
+    again = wire.serialize(b, channels=("advantage", "reward"), meta_blob=meta_blob if meta else None,
+                           meta_off=meta_off if meta else None)
+    assert again.cpu().numpy().tobytes() == blob.tobytes()
