@@ -194,6 +194,12 @@ size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_sr
 dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
                               const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream);
 
+/* Per-iteration reward statistics, replacing detail::record_reward_stats
+ * (worker.hpp:177-190): out[0..3) = {count, sum, sum of squares} of the
+ * rollouts' "reward" channel (device f64), so the cluster reduction of
+ * aggregate_metrics (worker.hpp:275-325) is one scalar all-reduce. */
+dfx_status dfx_reward_stats(const dfx_packed* b, double* out, dfx_stream stream);
+
 /* Device-side error flags written by kernels (e.g. an empty record seen by the
  * fused GRPO path). Reads flags (device int32) and returns the status. Syncs. */
 dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream);

@@ -933,3 +933,47 @@ dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------------------------
+// Per-iteration reward statistics: detail::record_reward_stats (worker.hpp:177-190) on the
+// device -- count, sum and sum of squares of the rollouts' "reward" channel -- so aggregate_metrics
+// (worker.hpp:275-325) becomes one scalar all-reduce instead of a JSON gather. One block, fixed-shape tree:
+// deterministic (f64; the reference's sequential order is not reproduced bit for bit).
+// ---------------------------------------------------------------------------------------------------------------
+namespace dfx {
+__global__ void __launch_bounds__(1024) reward_stats_kernel(int64_t n, const double* __restrict__ reward,
+                                                            double* __restrict__ out) {
+  __shared__ double sh[32][2];
+  double s = 0.0, q = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    const double r = reward[i];
+    s += r;
+    q = fma(r, r, q);
+  }
+  s = warp_sum(s);
+  q = warp_sum(q);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[wid][0] = s;
+    sh[wid][1] = q;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    s = warp_sum(sh[lane][0]);
+    q = warp_sum(sh[lane][1]);
+    if (lane == 0) {
+      out[0] = (double)n;
+      out[1] = s;
+      out[2] = q;
+    }
+  }
+}
+}  // namespace dfx
+
+extern "C" dfx_status dfx_reward_stats(const dfx_packed* b, double* out, dfx_stream stream) {
+  if (!b || !out) return fail(DFX_INVALID_ARGUMENT, "dfx_reward_stats: null argument");
+  if (!b->reward) return fail(DFX_MISSING_CHANNEL, "missing channel 'reward'");
+  reward_stats_kernel<<<1, 1024, 0, stream>>>(b->n_rollouts, b->reward, out);
+  DFX_LAUNCH_CHECK("reward_stats_kernel");
+  return DFX_OK;
+}

@@ -309,6 +309,31 @@ def ppo_loss_sources(sources: list, ctx: StageContext, loss_group_off=None, adv_
     return res
 
 
+def reward_stats(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
+    """detail::record_reward_stats (worker.hpp:177-190) on the device: f64 {count, sum, sum of squares} of the
+    rollouts' 'reward' channel."""
+    _channel(batch, "reward")
+    out = torch.empty(3, dtype=torch.float64, device=batch.device)
+    st = batch.struct()
+    _abi.check(_abi.lib().dfx_reward_stats(C.byref(st), _ptr(out), ctx.cuda_stream(batch.device)))
+    return out
+
+
+def aggregate_metrics(stats: torch.Tensor, tokens: int, suppressed: int = 0, group=None) -> dict:
+    """aggregate_metrics (worker.hpp:275-325) as one scalar all-reduce: every rank contributes its reward stats,
+    generation tokens (TP-0 workers only, as the reference) and suppressed puts; every rank returns the cluster
+    reward mean / variance (E[r^2] - mean^2, the reference's entropy proxy) and totals."""
+    v = torch.cat([stats.to(torch.float64), torch.tensor([float(tokens), float(suppressed)], dtype=torch.float64,
+                                                         device=stats.device)])
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        torch.distributed.all_reduce(v, group=group)
+    n, s, q, t, sup = v.tolist()
+    mean = s / n if n else 0.0
+    var = q / n - mean * mean if n else 0.0
+    return {"reward_count": int(n), "reward_mean": mean, "reward_variance": var, "global_tokens": int(t),
+            "suppressed_total": int(sup)}
+
+
 def loss_dict(out_row: torch.Tensor) -> dict:
     vals = out_row.detach().cpu().tolist()
     return dict(zip(_abi.LOSS_OUT_FIELDS, vals))

@@ -289,3 +289,18 @@ def test_gae_shapes(O, dfx, case):
     assert wsg[2] == wref[2]
     if wref[2] > 0:
         assert_close_vec(wsg[:2], wref[:2], "whiten sums")
+
+
+@pytest.mark.parametrize("case", CASES[:3])
+def test_reward_stats(O, dfx, case):
+    """record_reward_stats (worker.hpp:177-190) on the device: count exact, sums to f64 reduction-order rounding."""
+    seed, R, n, kind, lo, hi = case
+    sb = make(O, seed, R, n, kind, lo, hi)
+    db = device_batch(dfx, sb)
+    got = dfx.reward_stats(db, dfx.StageContext()).cpu().numpy()
+    s = q = 0.0
+    for r in sb.reward.tolist():  # the reference's sequential accumulation
+        s += r
+        q += r * r
+    assert got[0] == len(sb.reward)
+    assert abs(got[1] - s) <= 1e-12 * abs(s) and abs(got[2] - q) <= 1e-12 * abs(q)

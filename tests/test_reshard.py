@@ -242,3 +242,35 @@ def test_two_gpu_lazy_reshard_fused_loss():
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("LAZY_OK") == 2, r.stdout[-2000:]
+
+
+def _metrics_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2507_13833_b200 as dfx
+        stats = torch.tensor([3.0 + rank, 1.5 * (rank + 1), 2.0 + rank], dtype=torch.float64)
+        q.put((rank, dfx.aggregate_metrics(stats, tokens=100 * (rank + 1), suppressed=rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_aggregate_metrics_gloo_world2(dfx):
+    """aggregate_metrics (worker.hpp:275-325) as one all-reduce: totals and reward mean/variance like rank 0 of
+    the reference computes them from the gathered per-rank sums."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + (os.getpid() % 500)
+    procs = [ctx.Process(target=_metrics_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, s, sq = 3.0 + 4.0, 1.5 + 3.0, 2.0 + 3.0
+    want = {"reward_count": 7, "reward_mean": s / n, "reward_variance": sq / n - (s / n) ** 2, "global_tokens": 300,
+            "suppressed_total": 1}
+    assert res[0] == res[1] == want

@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_wire.py -q -x -p no:cacheprovider 2>&1 | tail -15
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -3
