@@ -65,7 +65,16 @@ def both():
     torch.cuda.current_stream().wait_stream(side)
 
 
+def sm_and_ce():
+    """the loss kernel reads the remote run over NVLink while the copy engines pull the same bytes again"""
+    side.wait_stream(torch.cuda.current_stream())
+    pull(side)
+    dfx.ppo_loss_sources([remote], ctx, device=dev)
+    torch.cuda.current_stream().wait_stream(side)
+
+
 res = {
+    "sm_read_plus_ce_pull_ms": timeit(sm_and_ce),
     "loss_local+remote_ms": timeit(lambda: dfx.ppo_loss_sources(srcs, ctx, device=dev)),
     "loss_remote_only_ms": timeit(lambda: dfx.ppo_loss_sources([remote], ctx, device=dev)),
     "loss_local_only_ms": timeit(lambda: dfx.ppo_loss_sources([local], ctx, device=dev)),
@@ -75,6 +84,7 @@ res = {
 res["remote_MB"] = nbytes / 1e6
 res["sm_read_GBs"] = nbytes / res["loss_remote_only_ms"] / 1e6
 res["ce_GBs"] = nbytes / res["ce_pull_ms"] / 1e6
+res["sm_plus_ce_GBs"] = 2 * nbytes / res["sm_read_plus_ce_pull_ms"] / 1e6
 print(rank, {k: round(v, 4) for k, v in res.items()}, flush=True)
 store.worker_done(0)
 dist.barrier()
