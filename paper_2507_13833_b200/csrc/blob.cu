@@ -49,30 +49,32 @@ __device__ __forceinline__ void put_le(uint8_t* p, uint64_t v, int n) {
   for (int i = 0; i < n; ++i) p[i] = uint8_t(v >> (8 * i));
 }
 
-// Copy n bytes src -> dst (any alignment) with the block's threads: interior as aligned u32 stores built from two
-// aligned u32 loads and a funnel shift, the partial words at either end byte by byte.
+// Copy n bytes src -> dst (any alignment) with the block's threads. The 16-byte-aligned interior of dst is written
+// with 128-bit stores, each assembled from five aligned 32-bit source words with funnel shifts; the bytes before
+// and after it byte by byte (they may share a word with a neighbouring writer).
 __device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
   if (n == 0) return;
   const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst), d1 = d0 + n;
-  const uintptr_t a0 = (d0 + 3) & ~uintptr_t(3), a1 = d1 & ~uintptr_t(3);
-  if (a1 <= a0) {  // shorter than one aligned word
+  const uintptr_t a0 = (d0 + 15) & ~uintptr_t(15), a1 = d1 & ~uintptr_t(15);
+  if (a1 <= a0) {  // no whole aligned 16-byte unit
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
     return;
   }
   const uint64_t head = a0 - d0, tail = d1 - a1;
   if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
   if (threadIdx.x < tail) dst[n - tail + threadIdx.x] = src[n - tail + threadIdx.x];
-  // word w of the interior covers source bytes [head + 4w, head + 4w + 4)
-  const uint8_t* s = src + head;
-  const uintptr_t sa = reinterpret_cast<uintptr_t>(s);
+  // unit u covers source bytes [head + 16u, head + 16u + 16)
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src + head);
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
   const uint32_t sh = uint32_t(sa & 3u) * 8u;
-  uint32_t* dw = reinterpret_cast<uint32_t*>(a0);
-  const uint64_t nw = (a1 - a0) / 4;
-  if (sh == 0) {
-    for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x) dw[w] = __ldg(sw + w);
-  } else {
-    for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x) dw[w] = __funnelshift_r(__ldg(sw + w), __ldg(sw + w + 1), sh);
+  uint4* dv = reinterpret_cast<uint4*>(a0);
+  const uint64_t nu = (a1 - a0) / 16;
+  for (uint64_t u = threadIdx.x; u < nu; u += blockDim.x) {
+    const uint32_t* w = sw + 4 * u;
+    const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
+    const uint32_t w4 = sh ? __ldg(w + 4) : 0u;
+    dv[u] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                       __funnelshift_r(w3, w4, sh));
   }
 }
 
