@@ -52,9 +52,11 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--records", type=int, default=None, help="prompts per GPU (default: the workload's)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5", "c4"],
                     help="c2: 1024 prompts x 16 x U[1,4096] per GPU (weak scaling, the headline); c5: BASELINE "
-                         "config 5, 4096 prompts x 16 x skewed <=16k tokens split over the GPUs (strong scaling)")
+                         "config 5, 4096 prompts x 16 x skewed <=16k tokens split over the GPUs (strong scaling); "
+                         "c4: BASELINE config 4, the DataBuffer round trip dp8 -> dp4 (tp2) -> dp8 of a 16.8M-token "
+                         "batch (16 B/token payload) split over the GPUs, one DataBuffer per GPU")
     ap.add_argument("--workers", type=int, default=8,
                     help="box placement: logical workers (the reference's W); N=8 GPUs with 8 workers puts TP "
                          "partners on different GPUs -- --workers 4 on 4 GPUs previews that path")
@@ -74,7 +76,7 @@ class ClockSampler:
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, index: int, period_s: float = 0.005):
-        self.samples, self.reasons = [], set()
+        self.samples, self.mem_samples, self.reasons = [], [], set()
         self.max_mhz = None
         self._stop = threading.Event()
         self._period = period_s
@@ -90,6 +92,7 @@ class ClockSampler:
     def _sample(self):
         nv = self._nv
         self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        self.mem_samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_MEM))
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
         for bit, name in self.REASONS.items():
             if r & bit and bit != 0x1:
@@ -120,6 +123,7 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "mem_mhz": statistics.median(self.mem_samples) if self.mem_samples else None,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
@@ -379,6 +383,102 @@ def run_dfx(args):
         dist.destroy_process_group()
 
 
+def run_c4(args):
+    """BASELINE config 4: the inter-stage reshard round trip DP 8 -> 4 (tp 2) -> 8 of a 16.8M-token rollout batch
+    (1024 prompts x 16 x 1024 tokens; payload token_id, lp, old_lp, ref_lp = 16 B/token, plus reward / advantage),
+    one DataBuffer per GPU (B = N stores; logical world 8, or 16 at N = 8 where one worker per GPU cannot host a
+    tp-2 group), materialized consumer batches (get() semantics): copy-engine pulls over NVLink + unpack."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_13833_b200 as dfx
+    from paper_2507_13833_b200.reshard import Layout, Topology
+    from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    meta = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        meta = dist.new_group(backend="gloo")
+    logical = 16 if world == 8 else 8
+    W = logical // world
+    topo = Topology.box(logical, 1) if world == 1 else Topology.store_per_gpu(world, W)
+    dp = logical
+    stages = {"s": StoreStagePlan(Layout(dp, 1), Layout(dp // 2, 2)), "t": StoreStagePlan(Layout(dp // 2, 2), Layout(dp, 1))}
+    store = DeviceBufferStore(topo, rank, stages, meta_group=meta)
+    R = 1024 // world
+    batch = dfx.PackedBatch.synthetic(11, R, 16, dfx.TokenDist("constant", 1024), device=dev, first_id=rank * R,
+                                      streams=("token_id", "lp", "old_lp", "ref_lp"))
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), batch, dfx.StageContext())
+    local_p = [p for p in range(dp) if topo.gpu_of_worker[p] == rank]
+    per = R // len(local_p)
+    it = [0]
+    moved = [0]
+
+    def step():
+        i = it[0]
+        for j, p in enumerate(local_p):
+            store.put("s", i, p, 0, batch.view_records(j * per, (j + 1) * per))
+        cb = store.ensure_ready("s", i, Layout(dp // 2, 2))
+        for k, d in enumerate(cb.groups):
+            for t in range(2):
+                if topo.gpu_of_worker[2 * d + t] == rank:
+                    store.put("t", i, d, t, cb.group_view(d))
+        cb2 = store.ensure_ready("t", i, Layout(dp, 1))
+        moved[0] = cb.bytes_recv + cb2.bytes_recv
+        for _ in store.local_workers:
+            store.worker_done(i)
+        it[0] += 1
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    steps = max(1, args.steps)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0.record()
+        for _ in range(steps):
+            step()
+        s1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = s0.elapsed_time(s1) / steps
+    mv = float(moved[0])
+    if world > 1:
+        t = torch.tensor([ms, mv], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, mv = float(t[0].item()), float(t[1].item())
+    tokens = batch.token_span * world
+    ach = mv / (ms / 1e3) / 1e9
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(tokens / (ms / 1e3), 1), "unit": UNIT, "n_gpus": world,
+                "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 5), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bytes (bit-exact reshard)",
+                "data": "synthetic (keyed SplitMix64, generated on device)",
+                "config": {"workload": f"C4: DataBuffer round trip dp{dp} -> dp{dp // 2} (tp2) -> dp{dp} of 1024 "
+                                       f"prompts x 16 x 1024 tokens (16.8M tokens, 16 B/token payload) over {world} GPU",
+                           "placement": f"one DataBuffer per GPU (B={topo.num_nodes}, W={topo.workers_per_node})",
+                           "materialized": True, "global_tokens": tokens},
+                "e2e": None, "gpu_launches": 2 * 2,
+                "roofline": {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                             "frac": round(ach / NVLINK_PEER_GBS, 4), "traffic": None,
+                             "kernel": "the whole round trip (copy-engine pulls + unpack_kernel)",
+                             "bytes_per_step_max_gpu": int(mv),
+                             "peak_source": "measured peer copy, 770 GB/s per direction (B200_PROFILING.md)"},
+                "cpu_baseline": None, "clocks": clk.result()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_e2e(args, dfx, batch, ctx, resh, dev, stream, world):
     """Public-API step with host buffers: pinned host -> H2D of every input array, the step, D2H of the results."""
     import torch
@@ -502,6 +602,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_c4(args)
     else:
         run_dfx(args)
 

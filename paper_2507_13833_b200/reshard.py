@@ -346,13 +346,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
 
     # 3. allocate the consumer batch
     R, S, T = rec_off[-1], roll_off[-1], tok_off[-1]
-    out = PackedBatch(R, S, 0, T, torch.empty(R, dtype=torch.int64, device=dev),
-                      torch.empty(R + 1, dtype=torch.int32, device=dev), torch.empty(S, dtype=torch.int32, device=dev),
-                      torch.empty(S + 1, dtype=torch.int64, device=dev),
-                      {c: torch.empty(S, dtype=torch.float64, device=dev) for c in ch_names},
-                      {k: torch.empty(padded_len(T), dtype=dt, device=dev) for k, dt in stream_specs.items()})
-    for t in out.streams.values():
-        t[T:].zero_()
+    out = _alloc_batch(R, S, T, ch_names, stream_specs, dev)
     t_ = _mark("alloc", t_)
 
     metas = []
@@ -448,6 +442,24 @@ def _device_barrier(group, dev):
     if t is None:
         t = _BARRIER[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
     torch.distributed.all_reduce(t, group=group)
+
+
+def _alloc_batch(R, S, T, ch_names, stream_specs, dev) -> PackedBatch:
+    """A consumer batch carved out of ONE device allocation (16-byte aligned arrays): one allocator call instead
+    of one per array. The stream padding past T is left as is: kernels discard out-of-range lanes."""
+    specs = [("ids", torch.int64, R), ("go", torch.int32, R + 1), ("rg", torch.int32, S), ("cu", torch.int64, S + 1)]
+    specs += [("c:" + c, torch.float64, S) for c in ch_names]
+    specs += [("s:" + k, dt, padded_len(T)) for k, dt in stream_specs.items()]
+    offs, off = {}, 0
+    for name, dt, n in specs:
+        off = (off + 15) & ~15
+        offs[name] = off
+        off += n * torch.empty(0, dtype=dt).element_size()
+    buf = torch.empty(off + 16, dtype=torch.uint8, device=dev)
+    arr = {name: buf[offs[name]:offs[name] + n * torch.empty(0, dtype=dt).element_size()].view(dt)
+           for name, dt, n in specs}
+    return PackedBatch(R, S, 0, T, arr["ids"], arr["go"], arr["rg"], arr["cu"],
+                       {c: arr["c:" + c] for c in ch_names}, {k: arr["s:" + k] for k in stream_specs})
 
 
 def _export(t: torch.Tensor):

@@ -32,3 +32,7 @@ run n4 4
 run n4_w4 4 --workers 4
 run n2_w2 2 --workers 2
 run n4_store 4 --placement store
+run c4_n1 1 --workload c4 --steps 20
+run c4_n2 2 --workload c4 --steps 20
+run c4_n4 4 --workload c4 --steps 20
+run c5_n4 4 --workload c5 --steps 20
