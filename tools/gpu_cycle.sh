@@ -3,6 +3,7 @@
 # usage (on the box): bash tools/gpu_cycle.sh TAG [KERNEL_REGEX] [PROF_ARGS]
 TAG=${1:-run}; KRE=${2:-loss_slots}; PARGS=${3:-"--steps 2"}
 mkdir -p gpurun_out
+python paper_2507_13833_b200/build.py > /dev/null || exit 1  # never measure a stale libdfx.so
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo pytest_exit=$?; tail -3 gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python bench.py > gpurun_out/bench_$TAG.log 2>&1

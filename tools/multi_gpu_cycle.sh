@@ -4,6 +4,7 @@
 # partners on different GPUs), and the store-per-GPU placement. JSON lines -> gpurun_out/multi_<tag>_*.json
 TAG=${1:-run}
 mkdir -p gpurun_out
+python paper_2507_13833_b200/build.py > /dev/null || exit 1  # never measure a stale libdfx.so
 timeout 600 python -m pytest tests/test_reshard.py -q -x -m gpu -p no:cacheprovider 2>&1 | tail -2
 run() {  # name N extra...
   local name=$1 n=$2; shift 2
