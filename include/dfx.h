@@ -326,6 +326,9 @@ dfx_status dfx_blob_unpack(const uint8_t* blob, int64_t n_rollouts, const int64_
 dfx_status dfx_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, uint64_t* offset_out);
 dfx_status dfx_ipc_open(const void* handle, size_t handle_bytes, void** base);
 dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream stream);
+/* n copies (dst[i] <- src[i], bytes[i]; addresses as integers, device or peer-mapped) in one call. */
+dfx_status dfx_copy_batch(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
+                          dfx_stream stream);
 
 /* ---------------------------------------------------------------------------
  * Timing helpers (cudaEvent_t as void*), so ctypes callers can bracket a

@@ -117,4 +117,14 @@ dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream s
   return DFX_OK;
 }
 
+dfx_status dfx_copy_batch(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
+                          dfx_stream stream) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (bytes[i] == 0) continue;
+    DFX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst[i]), reinterpret_cast<const void*>(src[i]), bytes[i],
+                             cudaMemcpyDefault, stream));
+  }
+  return DFX_OK;
+}
+
 }  // extern "C"

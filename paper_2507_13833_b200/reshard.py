@@ -75,6 +75,8 @@ def _declare():
     L.dfx_ipc_open.argtypes = [P, C.c_size_t, C.POINTER(C.c_void_p)]
     L.dfx_ipc_open.restype = C.c_int32
     L.dfx_copy_async.argtypes = [P, P, C.c_size_t, P]
+    L.dfx_copy_batch.argtypes = [C.c_int64, P, P, P, P]
+    L.dfx_copy_batch.restype = C.c_int32
     L.dfx_copy_async.restype = C.c_int32
     L._reshard_declared = True
     return L
@@ -243,7 +245,8 @@ def _src_slices(plan: Plan, sources: dict):
 
 
 def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, meta_group=None,
-             transport: str = "pull", lazy: bool = False) -> ConsumerBatch:
+             transport: str = "pull", lazy: bool = False, templates: dict | None = None,
+             template_key=None) -> ConsumerBatch:
     """Run the reshard on this rank. sources: {producer dp rank: (PackedBatch, first record of that group in it)}
     for every locally held producer group. schema: (stream name -> dtype, channel names), needed only on ranks
     that hold no producer group. Collective across the ranks of `group` (torch.distributed NCCL group) when
@@ -255,7 +258,10 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     transport "nccl": grouped NCCL send/recv of 16-aligned token ranges + packed metadata (dfx_reshard_pack).
     lazy (pull transport): no consumer batch is built; remote segments stay in the producers' memory as
     RemoteSource runs that the consumer's kernels read over NVLink (dfx_ppo_loss_multi), local segments are views.
-    The caller runs ConsumerBatch.release() after its last read (the second device barrier)."""
+    The caller runs ConsumerBatch.release() after its last read (the second device barrier).
+    templates / template_key (pull, materialized): the store's cache of exchange templates, keyed by the producer
+    sizes and every rank's producer-batch signature; on a hit the table all-gather, the per-segment bookkeeping
+    and the consumer's host metadata are reused -- one batched copy call, one unpack, two barriers."""
     L = _declare()
     rank = plan.rank
     for p in plan.local_src:
@@ -273,6 +279,10 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     loc = _src_slices(plan, sources)
     distributed = plan.cross and _distributed(group)
     pull = distributed and transport == "pull"
+    tmpl = templates.get(template_key) if (templates is not None and pull and not lazy) else None
+    if tmpl is not None:
+        tmpl["hits"] = tmpl.get("hits", 0) + 1
+        return _exchange_from_template(tmpl, L, dev, st, group)
 
     # 1. per-segment table filled by the owner: rollouts, tokens, first token mod 16 (NCCL alignment),
     #    and (pull) the absolute token / rollout / record offsets in the owner's arrays
@@ -420,7 +430,52 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     t_ = _mark("unpack", t_)
     # host offsets of the consumer batch are fetched lazily (PackedBatch.ensure_host_meta): no D2H here
     out.host_group_off, out.host_cu = None, None
-    return ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
+    cbatch = ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
+    if pull and templates is not None and template_key is not None:
+        # record this exchange as a template: every copy as (stream, offset in the consumer stream, source
+        # address, bytes), the unpack segments, and (after one D2H, only now) the consumer's host offsets
+        copies = []
+        for i in order:
+            if i in loc:
+                b, r0, r1, s0, s1, t0, t1 = loc[i]
+                for k, t in out.streams.items():
+                    esz = t.element_size()
+                    copies.append((k, dst[i][2] * esz, b.streams[k].data_ptr() + t0 * esz, (t1 - t0) * esz))
+            else:
+                n_roll, n_tok, _, t0, s0, r0 = (int(x) for x in sizes[i])
+                addr = peer_addr[(plan.src_rank[plan.segs[i][1]], plan.segs[i][1])]
+                for k, t in out.streams.items():
+                    esz = t.element_size()
+                    copies.append((k, dst[i][2] * esz, addr["s:" + k] + t0 * esz, n_tok * esz))
+        out.ensure_host_meta()
+        templates[template_key] = {"R": R, "S": S, "T": T, "ch": list(ch_names), "specs": dict(stream_specs),
+                                   "copies": copies, "metas": (SegMeta * len(metas))(*metas), "n_metas": len(metas),
+                                   "groups": groups, "rec_off": rec_off, "roll_off": roll_off, "sent": sent,
+                                   "recv": recv_b, "h_go": out.host_group_off, "h_cu": out.host_cu}
+        if len(templates) > 8:
+            templates.pop(next(iter(templates)))
+    return cbatch
+
+
+def _exchange_from_template(tm: dict, L, dev, st, group) -> ConsumerBatch:
+    """A materialized pull whose producers are exactly those of the template (same memory, extents and
+    placement on every rank): fresh consumer buffers, the recorded copies in one call, one unpack."""
+    out = _alloc_batch(tm["R"], tm["S"], tm["T"], tm["ch"], tm["specs"], dev)
+    base = {k: t.data_ptr() for k, t in out.streams.items()}
+    cp = tm["copies"]
+    dsts = np.array([base[k] + off for k, off, _, _ in cp], np.uint64)
+    srcs = np.array([a for _, _, a, _ in cp], np.uint64)
+    nbs = np.array([n for _, _, _, n in cp], np.uint64)
+    _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+    _abi.check(L.dfx_copy_batch(len(cp), dsts.ctypes.data, srcs.ctypes.data, nbs.ctypes.data, st.cuda_stream))
+    if tm["n_metas"]:
+        chp = (C.c_void_p * max(1, len(tm["ch"])))(*[out.channels[c].data_ptr() for c in tm["ch"]])
+        _abi.check(L.dfx_reshard_unpack(C.cast(tm["metas"], C.c_void_p), tm["n_metas"], len(tm["ch"]),
+                                        out.ids.data_ptr(), out.group_off.data_ptr(), out.roll_group.data_ptr(),
+                                        out.cu_seqlens.data_ptr(), C.cast(chp, C.c_void_p), st.cuda_stream))
+    _device_barrier(group, dev)  # peers may reuse their buffers once every consumer has pulled
+    out.host_group_off, out.host_cu = tm["h_go"], tm["h_cu"]
+    return ConsumerBatch(out, tm["groups"], tm["rec_off"], tm["roll_off"], False, tm["sent"], tm["recv"])
 
 
 def reuse_lazy(prev: ConsumerBatch, group) -> ConsumerBatch:

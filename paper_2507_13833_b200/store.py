@@ -63,6 +63,7 @@ class DeviceBufferStore:
         self._done: dict = {}
         self._plans: dict = {}       # (stage, consumed layout, counts) -> Plan
         self._templates: dict = {}   # stage -> (key, lazy ConsumerBatch) for reuse when nothing changed
+        self._mat_templates: dict = {}  # (plan key, signatures) -> materialized pull template (reshard.exchange)
         self.template_hits = 0
         self.low_water = 0
         self.suppressed = 0
@@ -109,7 +110,7 @@ class DeviceBufferStore:
         counts = [e.by_group[p].n_records if p in e.by_group else 0 for p in range(sp.produced.dp)]
         # every rank must agree on the producer group sizes; ranks only know their own -> the plan needs them.
         # One small host all-gather carries the counts and a signature of every rank's producer batches.
-        sig = _signature([e.by_group[p] for p in local]) if lazy else 0
+        sig = _signature([e.by_group[p] for p in local]) if (lazy or self.transport == "pull") else 0
         counts, sigs = self._agree_counts(counts, local, sig)
         pkey = (stage, to, tuple(counts))
         plan = self._plans.get(pkey)
@@ -125,7 +126,8 @@ class DeviceBufferStore:
             self.template_hits += 1
         else:
             e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
-                               transport=self.transport, lazy=lazy)
+                               transport=self.transport, lazy=lazy, templates=self._mat_templates,
+                               template_key=tkey)
             if lazy and e.ready.sources is not None:
                 self._templates[stage] = (tkey, e.ready)
         e.consumed = to

@@ -39,18 +39,25 @@ for name, transport in (("dense", "pull"), ("cross", "pull"), ("dense", "nccl"),
     store = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(Layout(dp_p, tp_p), Layout(dp_c, tp_c))},
                               meta_group=meta, transport=transport)
     per = 16 // dp_p
-    for p in range(dp_p):
-        for t in range(tp_p):
-            w = p * tp_p + t
+    for it in range(2):  # iteration 1 reuses the exchange template of iteration 0 (same producer batches)
+        for p in range(dp_p):
+            for t in range(tp_p):
+                w = p * tp_p + t
+                if topo.gpu_of_worker[w] == rank:
+                    store.put("s", it, p, t, full.view_records(p * per, (p + 1) * per))
+        cb = store.ensure_ready("s", it, Layout(dp_c, tp_c))
+        torch.cuda.synchronize()
+        for i, d in enumerate(cb.groups):
+            got = store.get("s", it, d, Layout(dp_c, tp_c))
+            blob = _blob_of(O, cb.batch, cb.rec_off[i], cb.rec_off[i + 1])
+            assert blob.tobytes() == g[f"{name}_blob_{d}"].tobytes(), (name, rank, d, it)
+            assert got.n_records == int(g[f"{name}_counts"][d])
+            assert got.host_cu is None or list(got.host_cu) == list(got.cu_seqlens.cpu().numpy())
+        for w in range(topo.world):
             if topo.gpu_of_worker[w] == rank:
-                store.put("s", 0, p, t, full.view_records(p * per, (p + 1) * per))
-    cb = store.ensure_ready("s", 0, Layout(dp_c, tp_c))
-    torch.cuda.synchronize()
-    for i, d in enumerate(cb.groups):
-        got = store.get("s", 0, d, Layout(dp_c, tp_c))
-        blob = _blob_of(O, cb.batch, cb.rec_off[i], cb.rec_off[i + 1])
-        assert blob.tobytes() == g[f"{name}_blob_{d}"].tobytes(), (name, rank, d)
-        assert got.n_records == int(g[f"{name}_counts"][d])
+                store.worker_done(it)
+    if transport == "pull" and cb.groups and not cb.zero_copy:
+        assert sum(t.get("hits", 0) for t in store._mat_templates.values()) == 1, name
     assert store.bytes_sent > 0 or not cb.groups, name
     print(f"rank {rank} {name}/{transport}: dests {cb.groups} sent {store.bytes_sent} recv {store.bytes_recv} zero_copy "
           f"{cb.zero_copy}", flush=True)
