@@ -326,6 +326,12 @@ dfx_status dfx_blob_unpack(const uint8_t* blob, int64_t n_rollouts, const int64_
 dfx_status dfx_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, uint64_t* offset_out);
 dfx_status dfx_ipc_open(const void* handle, size_t handle_bytes, void** base);
 dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream stream);
+/* Record metadata of a zero-copy view of records [r0, r1) of a batch, on the device: group_off rebased to the
+ * view's first rollout ([r1-r0+1]) and roll_group rebased to r0 ([n_roll] = group_off[r1]-group_off[r0]). */
+dfx_status dfx_view_meta(const int32_t* group_off, const int32_t* roll_group, int64_t r0, int64_t r1, int64_t n_roll,
+                         int32_t* group_off_out, int32_t* roll_group_out, dfx_stream stream);
+/* Same-device copy by a kernel (HBM to HBM on the SMs; the copy engines' D2D path is ~6x slower). */
+dfx_status dfx_copy_sm(void* dst, const void* src, size_t bytes, dfx_stream stream);
 /* n copies (dst[i] <- src[i], bytes[i]; addresses as integers, device or peer-mapped) in one call. */
 dfx_status dfx_copy_batch(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
                           dfx_stream stream);

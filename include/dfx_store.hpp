@@ -71,6 +71,57 @@ inline std::shared_ptr<uint8_t> device_alloc(int device, size_t bytes, bool zero
   });
 }
 
+// Size-bucketed free lists of device blocks per GPU: a block returns here when its last owner drops it, so a
+// steady-state reshard loop allocates nothing (cudaMalloc / cudaFree synchronise the device).
+class DevicePool : public std::enable_shared_from_this<DevicePool> {
+ public:
+  ~DevicePool() {
+    for (auto& kv : free_)
+      for (uint8_t* p : kv.second) {
+        cudaSetDevice(kv.first.first);
+        cudaFree(p);
+      }
+  }
+  std::shared_ptr<uint8_t> get(int device, size_t bytes) {
+    const size_t b = bytes <= (1u << 20) ? ((bytes + 4095) & ~size_t(4095)) : ((bytes + (2u << 20) - 1) & ~size_t((2u << 20) - 1));
+    uint8_t* p = nullptr;
+    {
+      std::lock_guard lk(mu_);
+      auto& fl = free_[{device, b}];
+      if (!fl.empty()) {
+        p = fl.back();
+        fl.pop_back();
+      }
+    }
+    if (!p) {
+      int prev = 0;
+      store_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+      store_cuda(cudaSetDevice(device), "cudaSetDevice");
+      void* q = nullptr;
+      store_cuda(cudaMalloc(&q, b), "cudaMalloc");
+      store_cuda(cudaSetDevice(prev), "cudaSetDevice");
+      p = static_cast<uint8_t*>(q);
+    }
+    std::weak_ptr<DevicePool> self = shared_from_this();
+    return std::shared_ptr<uint8_t>(p, [self, device, b](uint8_t* q) {
+      if (auto pool = self.lock()) {
+        std::lock_guard lk(pool->mu_);
+        pool->free_[{device, b}].push_back(q);
+      } else {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaFree(q);
+        cudaSetDevice(cur);
+      }
+    });
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<std::pair<int, size_t>, std::vector<uint8_t*>> free_;
+};
+
 // A device-resident packed batch: records [group_off[r], group_off[r+1]) of rollouts, rollouts
 // [cu[s], cu[s+1]) of tokens in ABSOLUTE token coordinates of the streams. Host copies of group_off / cu travel
 // with it (views and the placement need them, no device reads).
@@ -146,7 +197,7 @@ struct DeviceBatch {
   }
 
   // Zero-copy view of records [r0, r1): streams and channels shared, group_off / roll_group rebased.
-  DeviceBatch view(int64_t r0, int64_t r1) const {
+  DeviceBatch view(int64_t r0, int64_t r1, DevicePool* pool = nullptr, cudaStream_t stream = nullptr) const {
     if (r0 == 0 && r1 == n_records) return *this;
     DeviceBatch v;
     v.device = device;
@@ -156,23 +207,24 @@ struct DeviceBatch {
     v.n_rollouts = s1 - s0;
     v.h_cu.assign(h_cu.begin() + s0, h_cu.begin() + s1 + 1);
     v.h_group_off.resize(size_t(r1 - r0 + 1));
-    std::vector<int32_t> rg;
     for (int64_t r = r0; r <= r1; ++r) v.h_group_off[size_t(r - r0)] = h_group_off[size_t(r)] - s0;
-    for (int64_t r = r0; r < r1; ++r)
-      for (int32_t s = h_group_off[size_t(r)]; s < h_group_off[size_t(r + 1)]; ++s) rg.push_back(int32_t(r - r0));
     v.token_base = v.h_cu.front();
     v.token_span = v.h_cu.back() - v.h_cu.front();
     v.ids = ids + r0;
     v.cu = cu + s0;
     for (const auto& [n, p] : channels) v.channels[n] = p + s0;
     v.streams = streams;
-    auto go = device_alloc(device, v.h_group_off.size() * 4 + rg.size() * 4 + 4);
-    store_cuda(cudaMemcpy(go.get(), v.h_group_off.data(), v.h_group_off.size() * 4, cudaMemcpyHostToDevice), "H2D");
-    if (!rg.empty())
-      store_cuda(cudaMemcpy(go.get() + v.h_group_off.size() * 4, rg.data(), rg.size() * 4, cudaMemcpyHostToDevice),
-                 "H2D");
+    // rebased group_off / roll_group built on the device (no host round trip)
+    const size_t gob = size_t(r1 - r0 + 1) * 4 + size_t(s1 - s0) * 4 + 16;
+    auto go = pool ? pool->get(device, gob) : device_alloc(device, gob);
     v.group_off = reinterpret_cast<int32_t*>(go.get());
-    v.roll_group = reinterpret_cast<int32_t*>(go.get() + v.h_group_off.size() * 4);
+    v.roll_group = reinterpret_cast<int32_t*>(go.get() + ((size_t(r1 - r0 + 1) * 4 + 15) & ~size_t(15)));
+    int prev = 0;
+    store_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+    store_cuda(cudaSetDevice(device), "cudaSetDevice");
+    store_check(dfx_view_meta(group_off, roll_group, r0, r1, s1 - s0, v.group_off, v.roll_group, stream));
+    if (!stream) store_cuda(cudaStreamSynchronize(nullptr), "cudaStreamSynchronize");
+    store_cuda(cudaSetDevice(prev), "cudaSetDevice");
     v.keep.push_back(go);
     return v;
   }
@@ -192,9 +244,19 @@ class DeviceBufferStore {
   // num_nodes x workers_per_node logical workers, all in this process; gpu_of_worker[w] = CUDA device of worker w.
   DeviceBufferStore(uint32_t num_nodes, uint32_t workers_per_node, std::vector<int> gpu_of_worker,
                     std::map<std::string, StagePlan> stages)
-      : B_(num_nodes), W_(workers_per_node), gpu_(std::move(gpu_of_worker)), stages_(std::move(stages)) {
+      : B_(num_nodes), W_(workers_per_node), gpu_(std::move(gpu_of_worker)), stages_(std::move(stages)),
+        pool_(std::make_shared<DevicePool>()) {
     if (gpu_.size() != size_t(B_) * W_) throw StoreError(DFX_LAYOUT_ERROR, "gpu_of_worker must map every worker");
     std::set<int> devs(gpu_.begin(), gpu_.end());
+    for (int d : devs) {  // one copy / unpack stream per GPU for the store's lifetime
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(d);
+      cudaStream_t st;
+      store_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+      streams_[d] = st;
+      cudaSetDevice(prev);
+    }
     for (int a : devs)  // peer access between every pair of the box's GPUs (NVLink / NVSwitch)
       for (int b : devs)
         if (a != b) {
@@ -212,6 +274,13 @@ class DeviceBufferStore {
         }
   }
 
+  ~DeviceBufferStore() {
+    for (auto& kv : streams_) cudaStreamDestroy(kv.second);
+  }
+  DeviceBufferStore(const DeviceBufferStore&) = delete;
+  DeviceBufferStore& operator=(const DeviceBufferStore&) = delete;
+
+  // The batches put must be complete on the device (the store copies them on its own streams).
   bool put(const std::string& stage, uint32_t iteration, uint32_t dp, uint32_t tp, DeviceBatch batch) {
     std::unique_lock lk(mu_);
     const StagePlan& plan = stage_plan(stage);
@@ -359,12 +428,14 @@ class DeviceBufferStore {
         if (mine.size() == 1 && src.at(mine[0]->src_group).device == dev) {  // one local run: a view
           const DeviceBatch& b = src.at(mine[0]->src_group);
           out.emplace(std::make_pair(d, dev),
-                      b.view(int64_t(mine[0]->src_rec), int64_t(mine[0]->src_rec + mine[0]->count)));
+                      b.view(int64_t(mine[0]->src_rec), int64_t(mine[0]->src_rec + mine[0]->count), pool_.get(),
+                             streams_.at(dev)));
           continue;
         }
         out.emplace(std::make_pair(d, dev), assemble(dev, mine, src, copied));
       }
     }
+    for (auto& kv : streams_) store_cuda(cudaStreamSynchronize(kv.second), "cudaStreamSynchronize");
     std::lock_guard lk(mu_);
     copied_ += copied;
     return out;
@@ -395,8 +466,8 @@ class DeviceBufferStore {
     o.token_span = T;
     o.h_group_off = hgo;
     o.h_cu = hcu;
-    auto meta = device_alloc(dev, size_t(R) * 8 + size_t(R + 1) * 4 + size_t(S) * 4 + size_t(S + 1) * 8 +
-                                      first.channels.size() * size_t(S) * 8 + 64);
+    auto meta = pool_->get(dev, size_t(R) * 8 + size_t(R + 1) * 4 + size_t(S) * 4 + size_t(S + 1) * 8 +
+                                    first.channels.size() * size_t(S) * 8 + 64);
     o.keep.push_back(meta);
     uint8_t* m = meta.get();
     o.ids = reinterpret_cast<uint64_t*>(m);
@@ -412,15 +483,14 @@ class DeviceBufferStore {
     off += size_t(R + 1) * 4;
     o.roll_group = reinterpret_cast<int32_t*>(m + off);
     for (const auto& kv : first.streams) {
-      auto sm = device_alloc(dev, size_t(T) * kv.second.elem + 16 * kv.second.elem + 64, true);
+      auto sm = pool_->get(dev, size_t(T) * kv.second.elem + 16 * kv.second.elem + 64);  // padding: over-read slack
       o.keep.push_back(sm);
       o.streams[kv.first] = DeviceBatch::Stream{sm.get(), kv.second.elem};
     }
     int prev = 0;
     store_cuda(cudaGetDevice(&prev), "cudaGetDevice");
     store_cuda(cudaSetDevice(dev), "cudaSetDevice");
-    cudaStream_t st;
-    store_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaStream_t st = streams_.at(dev);
     std::vector<dfx_seg_meta> metas;
     int64_t dr = 0, ds = 0, dt = 0;
     for (const dfx_segment* sg : segs) {
@@ -431,9 +501,12 @@ class DeviceBufferStore {
       for (const auto& kv : b.streams) {
         const size_t e = kv.second.elem;
         if (t1 > t0) {
-          store_cuda(cudaMemcpyPeerAsync(o.streams.at(kv.first).base + size_t(dt) * e, dev, kv.second.base + size_t(t0) * e,
-                                         b.device, size_t(t1 - t0) * e, st),
-                     "cudaMemcpyPeerAsync");
+          uint8_t* to = o.streams.at(kv.first).base + size_t(dt) * e;
+          const uint8_t* from = kv.second.base + size_t(t0) * e;
+          if (b.device == dev)  // same GPU: an SM copy kernel (HBM rate), not the copy engine
+            store_check(dfx_copy_sm(to, from, size_t(t1 - t0) * e, st));
+          else                  // another GPU: a copy-engine pull over NVLink
+            store_cuda(cudaMemcpyPeerAsync(to, dev, from, b.device, size_t(t1 - t0) * e, st), "cudaMemcpyPeerAsync");
           copied += uint64_t(t1 - t0) * e;
         }
       }
@@ -455,9 +528,7 @@ class DeviceBufferStore {
     }
     store_check(dfx_reshard_unpack(metas.data(), int32_t(metas.size()), int32_t(dst_ch.size()), o.ids, o.group_off,
                                    o.roll_group, o.cu, dst_ch.data(), st));
-    store_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    cudaStreamDestroy(st);
-    store_cuda(cudaSetDevice(prev), "cudaSetDevice");
+    store_cuda(cudaSetDevice(prev), "cudaSetDevice");  // completion: the exchange synchronises every stream
     return o;
   }
 
@@ -471,6 +542,8 @@ class DeviceBufferStore {
   uint32_t low_water_ = 0;
   uint64_t suppressed_ = 0;
   uint64_t copied_ = 0;
+  std::shared_ptr<DevicePool> pool_;
+  std::map<int, cudaStream_t> streams_;
 };
 
 }  // namespace dfx

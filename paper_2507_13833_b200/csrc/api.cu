@@ -1,3 +1,4 @@
+#include <algorithm>
 // api.cu -- error plumbing and library identity for libdfx.
 #include <cstdio>
 #include <cstring>
@@ -114,6 +115,59 @@ dfx_status dfx_ipc_export(const void* ptr, void* handle_out, uint64_t* offset_ou
 dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream stream) {
   if (bytes == 0) return DFX_OK;
   DFX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream));
+  return DFX_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Same-device copy on the SMs (HBM -> HBM at ~3 TB/s; a copy-engine D2D copy runs at ~0.5 TB/s): 16-byte
+// vectors when both ends are 16-byte aligned, else 4-byte words, else bytes.
+__global__ void __launch_bounds__(256) copy_sm_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                      uint64_t n, int width) {
+  const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (uint64_t)gridDim.x * blockDim.x;
+  if (width == 16) {
+    for (uint64_t i = i0; i < n / 16; i += step)
+      reinterpret_cast<uint4*>(dst)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+    for (uint64_t i = (n / 16) * 16 + i0; i < n; i += step) dst[i] = src[i];
+  } else if (width == 4) {
+    for (uint64_t i = i0; i < n / 4; i += step) reinterpret_cast<uint32_t*>(dst)[i] = __ldcs(reinterpret_cast<const uint32_t*>(src) + i);
+    for (uint64_t i = (n / 4) * 4 + i0; i < n; i += step) dst[i] = src[i];
+  } else {
+    for (uint64_t i = i0; i < n; i += step) dst[i] = src[i];
+  }
+}
+// record metadata of a view of records [r0, r1): group_off rebased to its first rollout, roll_group to r0
+__global__ void __launch_bounds__(256) view_meta_kernel(const int32_t* __restrict__ go, const int32_t* __restrict__ rg,
+                                                        int64_t r0, int64_t r1, int32_t* __restrict__ go_out,
+                                                        int32_t* __restrict__ rg_out) {
+  const int32_t s0 = go[r0], s1 = go[r1];
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i <= r1 - r0; i += step) go_out[i] = go[r0 + i] - s0;
+  for (int64_t j = i0; j < s1 - s0; j += step) rg_out[j] = rg[s0 + j] - (int32_t)r0;
+}
+}  // namespace
+
+extern "C" {
+
+dfx_status dfx_view_meta(const int32_t* group_off, const int32_t* roll_group, int64_t r0, int64_t r1, int64_t n_roll,
+                         int32_t* group_off_out, int32_t* roll_group_out, dfx_stream stream) {
+  if (r1 < r0) return dfx::fail(DFX_INVALID_ARGUMENT, "dfx_view_meta: r1 < r0");
+  const int64_t n = std::max<int64_t>(r1 - r0 + 1, n_roll);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 1184);
+  view_meta_kernel<<<grid, 256, 0, stream>>>(group_off, roll_group, r0, r1, group_off_out, roll_group_out);
+  DFX_LAUNCH_CHECK("view_meta_kernel");
+  return DFX_OK;
+}
+
+dfx_status dfx_copy_sm(void* dst, const void* src, size_t bytes, dfx_stream stream) {
+  if (bytes == 0) return DFX_OK;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+  const int width = (a & 15u) == 0 ? 16 : (a & 3u) == 0 ? 4 : 1;
+  const uint64_t units = bytes / uint64_t(width) + 1;
+  const unsigned grid = (unsigned)std::min<uint64_t>((units + 255) / 256, 148ull * 8);
+  copy_sm_kernel<<<grid, 256, 0, stream>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes, width);
+  DFX_LAUNCH_CHECK("copy_sm_kernel");
   return DFX_OK;
 }
 
