@@ -10,18 +10,20 @@
 //
 // Three launches, all stream-ordered (graph-capturable):
 //   gae_prep_kernel    thread per rollout: sets the rollout-end bit of its last token in a token bitmap and
-//                      advances the look-back epoch (safe here: the previous scan has completed);
-//   gae_tile_kernel    single-pass decoupled look-back scan. One CTA per tile, NOT persistent: block b scans tile
-//                      n_tiles-1-b, so the tiles it looks back at belong to lower block indices, which are
-//                      dispatched first (the forward-progress argument of CUB's single-pass scan). Every input of
-//                      a tile -- r, V, mask, the end bits and the token after each thread's chunk -- is loaded
-//                      with independent loads at entry, so there is no dependent global load before the
-//                      look-back; each thread clears the end-bit byte it consumed, leaving the bitmap zero;
+//                      advances the look-back epoch (safe here: the previous scan has completed); it releases the
+//                      scan as a programmatic dependent launch, so the scan's loads overlap it;
+//   gae_smem_kernel    single-pass decoupled look-back scan. One CTA per 4096-token tile, NOT persistent: block b
+//                      scans tile n_tiles-1-b, so the tiles it looks back at belong to lower block indices, which
+//                      are dispatched first (the forward-progress argument of CUB's single-pass scan). The tile is
+//                      bulk-loaded (TMA) into shared memory; each thread owns 32 tokens; every input (r, V, mask,
+//                      end bits, the token after the tile) is read without any dependent global load before the
+//                      look-back, and each thread clears the end-bit word it consumed, leaving the bitmap zero;
 //   gae_finish_kernel  (whitening only) reduces the per-tile masked sums in tile order: deterministic.
 // Tile state is one 16-byte record per tile {f64 x ; f32 c ; u32 tag} written and polled with single relaxed
 // 128-bit accesses, so value and status are never seen out of order and no fence is needed (on sm_100 a gpu-scope
 // fence or acquire invalidates L1: CCTL.IVALL, measured as the top stall of a fenced version).
-// Arithmetic: f32 inside a thread's chunk of 8-16 tokens, f64 across chunks; outputs f32. HBM-bound: 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map.
+// Arithmetic: f32 inside a thread's chunk of 4 tokens / 32 tokens, f64 across threads; outputs f32. HBM-bound:
+// 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map. Design history: profiles/r01_gae_experiments.md.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -87,13 +89,6 @@ __global__ void __launch_bounds__(256) gae_prep_kernel(const int64_t* __restrict
 }
 
 // ---- the scan ---------------------------------------------------------------------------------------------------
-template <int TPT>
-struct TokVec {
-  float r[TPT], v[TPT];
-  uint32_t m;     // bit q: mask of token q
-  uint32_t last;  // bit q: token q ends its rollout
-};
-
 // Warp-parallel decoupled look-back (warp 0 of the block): the carry X = A at the first token after `tile`.
 __device__ __forceinline__ double gae_lookback(const GaeParams& p, int64_t tile, unsigned int F_AGG,
                                                unsigned int F_INC, int lane) {
@@ -126,196 +121,6 @@ __device__ __forceinline__ double gae_lookback(const GaeParams& p, int64_t tile,
     if (first < 32) return G.d;
   }
 }
-
-template <int THREADS, int TPT, int MINB, bool WHITEN>
-__global__ void __launch_bounds__(THREADS, MINB) gae_tile_kernel(GaeParams p) {
-  static_assert(TPT == 8 || TPT == 16, "TPT: 8 or 16 tokens per thread");
-  constexpr int TILE = THREADS * TPT, NW = THREADS / 32;
-  __shared__ Aff s_warp[NW];
-  __shared__ double s_X;
-  __shared__ double s_red[NW][3];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = p.n_tiles - 1 - (int64_t)blockIdx.x;
-  const int64_t T0 = p.base + tile * TILE;
-  const int64_t rd_end = (p.end + 15) & ~int64_t(15);
-  const int64_t c0 = T0 + (int64_t)tid * TPT;
-
-  // 0. keep HBM busy while this CTA computes and looks back: one thread bulk-prefetches into L2 the inputs of the
-  //    tile that the CTA replacing this one (pf_dist blocks later) will scan, so its loads hit L2
-  if (tid == 0 && p.pf_dist > 0 && tile >= p.pf_dist) {
-    const int64_t T0p = p.base + (tile - p.pf_dist) * TILE;
-    const uint32_t n = (uint32_t)min((int64_t)TILE, rd_end - T0p);
-    l2_prefetch(p.rew + T0p, 4u * n);
-    l2_prefetch(p.val + T0p, 4u * n);
-    l2_prefetch(p.mask + T0p, n);
-  }
-  // 1. every load up front, all independent: r, V, mask, end bits of this thread's TPT tokens, and (lane 31)
-  //    V / mask of the token after the chunk. Out-of-range tokens read as zeros and are identities below.
-  TokVec<TPT> x;
-  x.m = 0u;
-  x.last = 0u;
-  float vn = 0.0f;
-  uint32_t mn = 0u;
-  if (c0 < rd_end) {
-#pragma unroll
-    for (int q = 0; q < TPT; q += 4) {
-      const float4 a = ldg_stream_f4(p.rew + c0 + q);
-      const float4 b = ldg_stream_f4(p.val + c0 + q);
-      x.r[q] = a.x; x.r[q + 1] = a.y; x.r[q + 2] = a.z; x.r[q + 3] = a.w;
-      x.v[q] = b.x; x.v[q + 1] = b.y; x.v[q + 2] = b.z; x.v[q + 3] = b.w;
-    }
-    uint32_t mw[TPT / 4];
-#pragma unroll
-    for (int q = 0; q < TPT / 4; ++q) mw[q] = ldg_stream_u32(p.mask + c0 + 4 * q);
-    uint8_t* eb = p.ends + ((c0 - p.base) >> 3);
-    if (TPT == 8) {
-      x.last = *eb;
-      if (x.last) *eb = 0;  // leave the bitmap zero for the next call
-    } else {
-      x.last = *reinterpret_cast<uint16_t*>(eb);
-      if (x.last) *reinterpret_cast<uint16_t*>(eb) = 0;
-    }
-#pragma unroll
-    for (int q = 0; q < TPT / 4; ++q)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) x.m |= (((mw[q] >> (8 * k)) & 0xffu) ? 1u : 0u) << (4 * q + k);
-  } else {
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) x.r[q] = x.v[q] = 0.0f;
-  }
-  if (lane == 31 && c0 + TPT < p.end) {
-    vn = __ldg(p.val + c0 + TPT);
-    mn = __ldg(p.mask + c0 + TPT) ? 1u : 0u;
-  }
-  {
-    const float v1 = __shfl_down_sync(kFull, x.v[0], 1);
-    const uint32_t m1 = __shfl_down_sync(kFull, x.m & 1u, 1);
-    if (lane < 31) {
-      vn = v1;
-      mn = m1;
-    }
-  }
-  const unsigned int epoch = (unsigned int)*((volatile unsigned long long*)(p.ticket + 2));
-  const unsigned int F_AGG = (epoch << 2) | 1u, F_INC = (epoch << 2) | 2u;
-
-  // 2. per-token maps, hoisted into bit masks: token q is f_q(X) = d_q + c_q X with c_q = gl if bit q of `link`
-  //    (the next token is in the same rollout and unmasked) else 0; `ident` marks tokens outside the batch
-  //    (boundary threads only), which pass the carry through unchanged. Within a thread's chunk the maps are
-  //    composed and applied in f32 (TPT steps, a few ulp); everything that crosses chunks -- warp and block scans,
-  //    tile records, carries -- is f64.
-  constexpr uint32_t kAll = (1u << TPT) - 1u;
-  const uint32_t link = (((x.m >> 1) | (mn << (TPT - 1))) & ~x.last) & kAll;
-  uint32_t ident = 0u;
-  if (!(c0 >= p.begin && c0 + TPT <= p.end)) {
-#pragma unroll
-    for (int q = 0; q < TPT; ++q)
-      if (c0 + q < p.begin || c0 + q >= p.end) ident |= 1u << q;
-  }
-  const float gam = (float)p.gamma, glf = (float)p.gl;
-  float d[TPT];
-  float Fd = 0.0f, Fc = 1.0f;  // thread map, composed right to left
-#pragma unroll
-  for (int q = TPT - 1; q >= 0; --q) {
-    const float vnext = q == TPT - 1 ? vn : x.v[q + 1];
-    const bool lk = (link >> q) & 1u;
-    const float dq = (lk ? fmaf(gam, vnext, x.r[q]) : x.r[q]) - x.v[q];
-    d[q] = dq;
-    Fd = lk ? fmaf(glf, Fd, dq) : dq;
-    Fc = lk ? Fc * glf : 0.0f;
-  }
-  if (ident) {  // boundary threads: recompose with the identities skipped
-    Fd = 0.0f;
-    Fc = 1.0f;
-#pragma unroll
-    for (int q = TPT - 1; q >= 0; --q) {
-      if ((ident >> q) & 1u) continue;
-      const bool lk = (link >> q) & 1u;
-      Fd = lk ? fmaf(glf, Fd, d[q]) : d[q];
-      Fc = lk ? Fc * glf : 0.0f;
-    }
-  }
-  // 3. warp suffix scan (f64), tile aggregate
-  Aff S{(double)Fd, (double)Fc};
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double od = __shfl_down_sync(kFull, S.d, o), oc = __shfl_down_sync(kFull, S.c, o);
-    if (lane + o < 32) S = compose(S, Aff{od, oc});
-  }
-  if (lane == 0) s_warp[wid] = S;
-  Aff E{__shfl_down_sync(kFull, S.d, 1), __shfl_down_sync(kFull, S.c, 1)};
-  if (lane == 31) E = Aff{0.0, 1.0};
-  __syncthreads();
-  // 4. publish + look-back (warp 0). A tile holding a rollout end has c == 0 and is inclusive at once; its carry
-  //    is still resolved, for the tokens after its last rollout end.
-  if (wid == 0) {
-    Aff tot{0.0, 1.0};
-#pragma unroll
-    for (int w = NW - 1; w >= 0; --w) tot = compose(s_warp[w], tot);
-    if (lane == 0) rec_store(p.rec + tile, tot.d, (float)tot.c, tot.c == 0.0 ? F_INC : F_AGG);
-    const double X = gae_lookback(p, tile, F_AGG, F_INC, lane);
-    if (lane == 0) {
-      if (tot.c != 0.0) rec_store(p.rec + tile, fma(tot.c, X, tot.d), 0.0f, F_INC);
-      s_X = X;
-    }
-  }
-  __syncthreads();
-  // 5. carry into this thread (f64), final pass in f32, stores four tokens at a time as soon as they are final
-  double Xd = s_X;
-#pragma unroll
-  for (int w = NW - 1; w >= 0; --w)
-    if (w > wid) Xd = fma(s_warp[w].c, Xd, s_warp[w].d);
-  float X = (float)fma(E.c, Xd, E.d);
-  float wa = 0.0f, wa2 = 0.0f;
-#pragma unroll
-  for (int g = TPT - 4; g >= 0; g -= 4) {
-    float oa[4], orr[4];
-#pragma unroll
-    for (int k = 3; k >= 0; --k) {
-      const int q = g + k;
-      const float A = ((link >> q) & 1u) ? fmaf(glf, X, d[q]) : d[q];
-      X = ((ident >> q) & 1u) ? X : A;
-      oa[k] = X;
-      orr[k] = X + x.v[q];
-      if (WHITEN) {
-        const float mw = ((x.m & ~ident) >> q) & 1u ? 1.0f : 0.0f;
-        wa = fmaf(mw, X, wa);
-        wa2 = fmaf(mw * X, X, wa2);
-      }
-    }
-    if (!ident) {
-      stg_stream_f4(p.adv + c0 + g, make_float4(oa[0], oa[1], oa[2], oa[3]));
-      stg_stream_f4(p.ret + c0 + g, make_float4(orr[0], orr[1], orr[2], orr[3]));
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (!((ident >> (g + k)) & 1u)) {
-          p.adv[c0 + g + k] = oa[k];
-          p.ret[c0 + g + k] = orr[k];
-        }
-      }
-    }
-  }
-  if (WHITEN) {  // per-tile masked sums, reduced in tile order by gae_finish_kernel
-    double wm = (double)__popc(x.m & ~ident & kAll);
-    double wad = warp_sum((double)wa), wa2d = warp_sum((double)wa2);
-    wm = warp_sum(wm);
-    if (lane == 0) {
-      s_red[wid][0] = wad;
-      s_red[wid][1] = wa2d;
-      s_red[wid][2] = wm;
-    }
-    __syncthreads();
-    if (tid < 3) {
-      double t3 = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) t3 += s_red[w][tid];
-      p.part[(int64_t)tid * p.n_tiles + tile] = t3;
-    }
-  }
-}
-
-
-
 
 // ---------------------------------------------------------------------------------------------------------------
 // Shared-memory tiles (default): a tile of THREADS*32 tokens is bulk-loaded (TMA) into shared memory and each
@@ -564,7 +369,7 @@ int64_t gae_tiles(int64_t token_base, int64_t token_span, int64_t tile) {
   return (token_base + token_span - base + tile - 1) / tile;
 }
 
-constexpr int64_t kGaeMinTile = 2048;  // smallest tile of any variant (workspace sizing)
+constexpr int64_t kGaeMinTile = 2048;  // smallest tile of any variant (s64: 64 x 32 tokens; workspace sizing)
 
 struct GaeWs {
   size_t ticket, rec, part, ends, bytes;
@@ -582,15 +387,14 @@ GaeWs gae_ws_layout(int64_t token_span) {
   return w;
 }
 
-// Tuning knob (benchmarking only): DFX_GAE_VARIANT = s128 (default: shared-memory tiles of 128 x 32 tokens,
-// 5 CTAs/SM) | s128b4 | s128b6 | s256 | s64 | t128x16 | t256x8 | t256x16 (register tiles of THREADS x TPT tokens)
+// Tuning knob (benchmarking only): DFX_GAE_VARIANT = s128 (default: 128 threads x 32 tokens, 5 CTAs/SM) |
+// s128b4 | s256 | s64 (the register-tile designs it replaced are in profiles/r01_gae_experiments.md)
 inline int gae_variant() {
   static const int v = [] {
     const char* e = std::getenv("DFX_GAE_VARIANT");
     if (!e) return 0;
     const std::string s(e);
-    return s == "t256x8" ? 1 : s == "t256x16" ? 2 : s == "t128x16" ? 3 : s == "s256" ? 4 : s == "s64" ? 5 : s == "s128b4" ? 8
-           : s == "s128b6" ? 7 : 0;
+    return s == "s128b4" ? 1 : s == "s256" ? 2 : s == "s64" ? 3 : 0;
   }();
   return v;
 }
@@ -627,24 +431,6 @@ void gae_launch_smem(GaeParams& p, cudaStream_t st) {
   else cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, false>, p);
 }
 
-template <int THREADS, int TPT, int MINB>
-void gae_launch_tile(GaeParams& p, cudaStream_t st) {
-  p.n_tiles = gae_tiles(p.begin, p.end - p.begin, THREADS * TPT);
-  static thread_local int cached_dev = -1, resident = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev) {  // CTAs resident at once = how far ahead the next wave's tiles are
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_tile_kernel<THREADS, TPT, MINB, true>, THREADS, 0);
-    resident = sms * std::max(per_sm, 1);
-    cached_dev = dev;
-  }
-  static const int pf_env = std::getenv("DFX_GAE_PF") ? std::atoi(std::getenv("DFX_GAE_PF")) : 100;
-  p.pf_dist = (int64_t)resident * pf_env / 100;
-  if (p.whiten) gae_tile_kernel<THREADS, TPT, MINB, true><<<(unsigned)p.n_tiles, THREADS, 0, st>>>(p);
-  else gae_tile_kernel<THREADS, TPT, MINB, false><<<(unsigned)p.n_tiles, THREADS, 0, st>>>(p);
-}
 
 }  // namespace dfx
 
@@ -690,17 +476,12 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
                                                                           reinterpret_cast<uint32_t*>(p.ends), p.ticket);
   DFX_LAUNCH_CHECK("gae_prep_kernel");
   switch (gae_variant()) {
-    case 1: gae_launch_tile<256, 8, 4>(p, stream); break;
-    case 2: gae_launch_tile<256, 16, 2>(p, stream); break;
-    case 3: gae_launch_tile<128, 16, 4>(p, stream); break;
-    case 4: gae_launch_smem<256, 2>(p, stream); break;
-    case 5: gae_launch_smem<64, 8>(p, stream); break;
-    case 6: gae_launch_smem<128, 5>(p, stream); break;
-    case 7: gae_launch_smem<128, 6>(p, stream); break;
-    case 8: gae_launch_smem<128, 4>(p, stream); break;
+    case 1: gae_launch_smem<128, 4>(p, stream); break;
+    case 2: gae_launch_smem<256, 2>(p, stream); break;
+    case 3: gae_launch_smem<64, 8>(p, stream); break;
     default: gae_launch_smem<128, 5>(p, stream); break;
   }
-  DFX_LAUNCH_CHECK("gae_tile_kernel");
+  DFX_LAUNCH_CHECK("gae_smem_kernel");
   if (whiten) {
     gae_finish_kernel<<<1, 256, 0, stream>>>(p.part, p.n_tiles, whiten);
     DFX_LAUNCH_CHECK("gae_finish_kernel");

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for v in default s128b4; do
+for v in default s128b4 s256 s64; do
   DFX_GAE_VARIANT=$v timeout 120 python -m pytest tests/test_gpu_parity.py -q -x -k gae -p no:cacheprovider 2>&1 | tail -1
   DFX_GAE_VARIANT=$v timeout 60 python tools/gae_bench.py
   DFX_GAE_VARIANT=$v timeout 60 python tools/gae_bench.py --whiten
