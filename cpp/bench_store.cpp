@@ -47,23 +47,36 @@ int main(int argc, char** argv) {
     prod.push_back(dfx::DeviceBatch::upload(gpu[p], ids, go, cu, ch, st));
   }
   cudaDeviceSynchronize();
+  double t_ex_s = 0, t_ex_t = 0, t_rest = 0;
+  using clk = std::chrono::steady_clock;
+  auto since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   auto trip = [&](uint32_t it) {
+    auto a = clk::now();
     for (uint32_t p = 0; p < dp; ++p) store.put("s", it, p, 0, prod[p]);
-    std::map<uint32_t, dfx::DeviceBatch> mid;
-    for (uint32_t w = 0; w < logical; ++w) {  // every worker's get on its GPU (the first runs the exchange)
+    cudaSetDevice(gpu[0]);
+    store.ensure_ready("s", it, dfx::Layout{dp / 2, 2});  // the exchange (the first consumer's get runs it)
+    t_ex_s += since(a);
+    a = clk::now();
+    for (uint32_t w = 0; w < logical; ++w) {  // every worker's get on its GPU
       cudaSetDevice(gpu[w]);
       const uint32_t d = w / 2;
       dfx::DeviceBatch b = store.get("s", it, d, dfx::Layout{dp / 2, 2});
-      if (w % 2 == 0) mid.emplace(d, b);
       store.put("t", it, d, w % 2, b);
     }
+    t_rest += since(a);
+    a = clk::now();
+    store.ensure_ready("t", it, dfx::Layout{dp, 1});
+    t_ex_t += since(a);
+    a = clk::now();
     for (uint32_t w = 0; w < logical; ++w) {
       cudaSetDevice(gpu[w]);
       (void)store.get("t", it, w, dfx::Layout{dp, 1});
     }
     for (uint32_t w = 0; w < logical; ++w) store.worker_done(it);
+    t_rest += since(a);
   };
   for (uint32_t it = 0; it < 3; ++it) trip(it);
+  t_ex_s = t_ex_t = t_rest = 0;
   const uint64_t c0 = store.bytes_copied();
   const auto t0 = std::chrono::steady_clock::now();
   for (int it = 0; it < iters; ++it) trip(3 + it);
@@ -72,7 +85,9 @@ int main(int argc, char** argv) {
   const double copied = double(store.bytes_copied() - c0) / iters;  // all GPUs, local + peer
   std::printf("{\"workload\": \"C4 round trip dp%u -> dp%u (tp2) -> dp%u, 16.8M tokens x 16 B, B=%u W=%u, %d GPU, "
               "C++ device DataBuffer (one process)\", \"ms_per_trip\": %.4f, \"tokens_per_s\": %.4g, "
-              "\"bytes_copied_per_trip\": %.0f, \"copy_GBs_per_gpu\": %.1f}\n",
-              dp, dp / 2, dp, B, W, N, ms, 16777216.0 / (ms / 1e3), copied, copied / N / (ms / 1e3) / 1e9);
+              "\"bytes_copied_per_trip\": %.0f, \"copy_GBs_per_gpu\": %.1f, \"exchange_s_ms\": %.4f, "
+              "\"exchange_t_ms\": %.4f, \"other_ms\": %.4f}\n",
+              dp, dp / 2, dp, B, W, N, ms, 16777216.0 / (ms / 1e3), copied, copied / N / (ms / 1e3) / 1e9,
+              t_ex_s / iters, t_ex_t / iters, t_rest / iters);
   return 0;
 }

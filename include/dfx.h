@@ -332,6 +332,10 @@ dfx_status dfx_view_meta(const int32_t* group_off, const int32_t* roll_group, in
                          int32_t* group_off_out, int32_t* roll_group_out, dfx_stream stream);
 /* Same-device copy by a kernel (HBM to HBM on the SMs; the copy engines' D2D path is ~6x slower). */
 dfx_status dfx_copy_sm(void* dst, const void* src, size_t bytes, dfx_stream stream);
+/* n copies (dst[i] <- src[i], bytes[i]; addresses as integers, device or peer-mapped) by ONE kernel launch per
+ * 96 copies: local and NVLink-mapped sources copied concurrently by the SMs in 64 KB chunks. */
+dfx_status dfx_copy_many(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
+                         dfx_stream stream);
 /* n copies (dst[i] <- src[i], bytes[i]; addresses as integers, device or peer-mapped) in one call. */
 dfx_status dfx_copy_batch(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
                           dfx_stream stream);

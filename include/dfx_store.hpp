@@ -16,8 +16,8 @@
 // logical workers of the box in this process, each bound to a GPU (gpu_of_worker). The record placement is the
 // reference's computed natively as segments (dfx_reshard_segments); a consumer group that is one
 // run of one producer batch on its GPU is a zero-copy view, otherwise it is assembled on its GPU: token streams by
-// peer copies over NVLink (cudaMemcpyPeerAsync), record/rollout metadata rebased by dfx_reshard_unpack reading
-// the producer's arrays through peer access. Errors are dfx::StoreError carrying the dfx_status code that
+// one copy kernel per batch (dfx_copy_many: local HBM and peer memory over NVLink), record/rollout metadata
+// rebased by dfx_reshard_unpack reading the producer's arrays through peer access. Errors are dfx::StoreError carrying the dfx_status code that
 // include/dfx_distflow.hpp maps to the reference's exception types.
 #pragma once
 
@@ -492,6 +492,7 @@ class DeviceBufferStore {
     store_cuda(cudaSetDevice(dev), "cudaSetDevice");
     cudaStream_t st = streams_.at(dev);
     std::vector<dfx_seg_meta> metas;
+    std::vector<uint64_t> cp_dst, cp_src, cp_n;
     int64_t dr = 0, ds = 0, dt = 0;
     for (const dfx_segment* sg : segs) {
       const DeviceBatch& b = src.at(sg->src_group);
@@ -500,13 +501,10 @@ class DeviceBufferStore {
       const int64_t t0 = b.h_cu[size_t(s0)], t1 = b.h_cu[size_t(s1)];
       for (const auto& kv : b.streams) {
         const size_t e = kv.second.elem;
-        if (t1 > t0) {
-          uint8_t* to = o.streams.at(kv.first).base + size_t(dt) * e;
-          const uint8_t* from = kv.second.base + size_t(t0) * e;
-          if (b.device == dev)  // same GPU: an SM copy kernel (HBM rate), not the copy engine
-            store_check(dfx_copy_sm(to, from, size_t(t1 - t0) * e, st));
-          else                  // another GPU: a copy-engine pull over NVLink
-            store_cuda(cudaMemcpyPeerAsync(to, dev, from, b.device, size_t(t1 - t0) * e, st), "cudaMemcpyPeerAsync");
+        if (t1 > t0) {  // all of this batch's copies (local HBM or a peer over NVLink) go out in one launch
+          cp_dst.push_back(uint64_t(reinterpret_cast<uintptr_t>(o.streams.at(kv.first).base + size_t(dt) * e)));
+          cp_src.push_back(uint64_t(reinterpret_cast<uintptr_t>(kv.second.base + size_t(t0) * e)));
+          cp_n.push_back(uint64_t(t1 - t0) * e);
           copied += uint64_t(t1 - t0) * e;
         }
       }
@@ -526,6 +524,7 @@ class DeviceBufferStore {
       ds += s1 - s0;
       dt += t1 - t0;
     }
+    store_check(dfx_copy_many(int64_t(cp_n.size()), cp_dst.data(), cp_src.data(), cp_n.data(), st));
     store_check(dfx_reshard_unpack(metas.data(), int32_t(metas.size()), int32_t(dst_ch.size()), o.ids, o.group_off,
                                    o.roll_group, o.cu, dst_ch.data(), st));
     store_cuda(cudaSetDevice(prev), "cudaSetDevice");  // completion: the exchange synchronises every stream

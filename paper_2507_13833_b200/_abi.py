@@ -98,7 +98,7 @@ EXPORTS = ("dfx_last_error", "dfx_version", "dfx_grpo_advantage", "dfx_broadcast
            "dfx_gae_workspace_bytes", "dfx_gae", "dfx_ppo_loss_workspace_bytes", "dfx_ppo_loss",
            "dfx_ppo_loss_multi_workspace_bytes", "dfx_ppo_loss_multi", "dfx_check_flags",
            "dfx_synth_tokens", "dfx_serialize_plan", "dfx_serialize_records",
-           "dfx_blob_index", "dfx_blob_unpack", "dfx_reward_stats", "dfx_copy_batch", "dfx_copy_sm", "dfx_view_meta", "dfx_event_create", "dfx_event_destroy", "dfx_event_record", "dfx_event_elapsed_ms")
+           "dfx_blob_index", "dfx_blob_unpack", "dfx_reward_stats", "dfx_copy_batch", "dfx_copy_sm", "dfx_view_meta", "dfx_copy_many", "dfx_event_create", "dfx_event_destroy", "dfx_event_record", "dfx_event_elapsed_ms")
 
 
 def check(status: int) -> None:

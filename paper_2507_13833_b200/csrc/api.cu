@@ -146,9 +146,66 @@ __global__ void __launch_bounds__(256) view_meta_kernel(const int32_t* __restric
   for (int64_t i = i0; i <= r1 - r0; i += step) go_out[i] = go[r0 + i] - s0;
   for (int64_t j = i0; j < s1 - s0; j += step) rg_out[j] = rg[s0 + j] - (int32_t)r0;
 }
+// Many copies in one launch (sources in this GPU's HBM or mapped from a peer over NVLink): every copy is cut into
+// 64 KB chunks, block b copies chunk b (found by a search over the per-copy chunk prefix), 16-byte vectors when
+// both ends are aligned. Local and remote copies run concurrently on the SMs instead of serially on one copy
+// engine queue, with no per-copy launch cost.
+constexpr int kCopyMany = 96;
+constexpr uint64_t kCopyChunk = 65536;
+struct CopyMany {
+  int n;
+  uint64_t dst[kCopyMany], src[kCopyMany], bytes[kCopyMany], chunk0[kCopyMany + 1];
+};
+__global__ void __launch_bounds__(256) copy_many_kernel(CopyMany c) {
+  const uint64_t ch = blockIdx.x;
+  int lo = 0, hi = c.n;  // last copy with chunk0 <= ch
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (c.chunk0[mid] <= ch) lo = mid;
+    else hi = mid;
+  }
+  const uint64_t off = (ch - c.chunk0[lo]) * kCopyChunk;
+  const uint64_t n = min(kCopyChunk, c.bytes[lo] - off);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(c.dst[lo]) + off;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(c.src[lo]) + off;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+  if ((a & 15u) == 0) {
+    for (uint64_t i = threadIdx.x; i < n / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(dst)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+    for (uint64_t i = (n / 16) * 16 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else if ((a & 3u) == 0) {
+    for (uint64_t i = threadIdx.x; i < n / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(dst)[i] = __ldcs(reinterpret_cast<const uint32_t*>(src) + i);
+    for (uint64_t i = (n / 4) * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
 }  // namespace
 
 extern "C" {
+
+dfx_status dfx_copy_many(int64_t n, const uint64_t* dst, const uint64_t* src, const uint64_t* bytes,
+                         dfx_stream stream) {
+  for (int64_t i0 = 0; i0 < n; i0 += kCopyMany) {
+    CopyMany c{};
+    uint64_t chunks = 0;
+    for (int64_t i = i0; i < std::min<int64_t>(n, i0 + kCopyMany); ++i) {
+      if (bytes[i] == 0) continue;
+      c.dst[c.n] = dst[i];
+      c.src[c.n] = src[i];
+      c.bytes[c.n] = bytes[i];
+      c.chunk0[c.n] = chunks;
+      chunks += (bytes[i] + kCopyChunk - 1) / kCopyChunk;
+      ++c.n;
+    }
+    if (c.n == 0) continue;
+    c.chunk0[c.n] = chunks;
+    copy_many_kernel<<<(unsigned)chunks, 256, 0, stream>>>(c);
+    DFX_LAUNCH_CHECK("copy_many_kernel");
+  }
+  return DFX_OK;
+}
 
 dfx_status dfx_view_meta(const int32_t* group_off, const int32_t* roll_group, int64_t r0, int64_t r1, int64_t n_roll,
                          int32_t* group_off_out, int32_t* roll_group_out, dfx_stream stream) {

@@ -77,6 +77,8 @@ def _declare():
     L.dfx_copy_async.argtypes = [P, P, C.c_size_t, P]
     L.dfx_copy_batch.argtypes = [C.c_int64, P, P, P, P]
     L.dfx_copy_batch.restype = C.c_int32
+    L.dfx_copy_many.argtypes = [C.c_int64, P, P, P, P]
+    L.dfx_copy_many.restype = C.c_int32
     L.dfx_copy_async.restype = C.c_int32
     L._reshard_declared = True
     return L
@@ -467,7 +469,7 @@ def _exchange_from_template(tm: dict, L, dev, st, group) -> ConsumerBatch:
     srcs = np.array([a for _, _, a, _ in cp], np.uint64)
     nbs = np.array([n for _, _, _, n in cp], np.uint64)
     _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
-    _abi.check(L.dfx_copy_batch(len(cp), dsts.ctypes.data, srcs.ctypes.data, nbs.ctypes.data, st.cuda_stream))
+    _abi.check(L.dfx_copy_many(len(cp), dsts.ctypes.data, srcs.ctypes.data, nbs.ctypes.data, st.cuda_stream))
     if tm["n_metas"]:
         chp = (C.c_void_p * max(1, len(tm["ch"])))(*[out.channels[c].data_ptr() for c in tm["ch"]])
         _abi.check(L.dfx_reshard_unpack(C.cast(tm["metas"], C.c_void_p), tm["n_metas"], len(tm["ch"]),
