@@ -15,6 +15,9 @@
  *     allocate: scratch comes from a caller-provided workspace sized by the
  *     matching *_workspace_bytes() query. Calls are re-entrant across threads
  *     and devices (no global mutable state besides the error message).
+ *   - Kernels launch on the calling thread's current device, which must own
+ *     the stream and the (non-peer) buffers (cudaSetDevice first when one
+ *     thread drives several GPUs; the Python layer does this per batch).
  *   - There is no CPU fallback: without a CUDA device every compute call
  *     returns DFX_CUDA_ERROR.
  */

@@ -113,6 +113,23 @@ class StageContext:
 StageFn = Callable[[NodeSpec, PackedBatch, StageContext], None]
 
 
+def _on_batch_device(pos: int):
+    """libdfx launches on the calling thread's current device; run the wrapped op with the batch's device current
+    (like torch's DeviceGuard) so one process can drive batches on several GPUs."""
+    def deco(fn):
+        import functools
+
+        @functools.wraps(fn)
+        def run(*args, **kwargs):
+            dev = args[pos].device
+            if dev.type != "cuda" or dev.index == torch.cuda.current_device():
+                return fn(*args, **kwargs)
+            with torch.cuda.device(dev):
+                return fn(*args, **kwargs)
+        return run
+    return deco
+
+
 # ---- checks mirroring detail::require_rollouts / channel_of (functions.hpp:82-93) ---------------
 def _require_rollouts(batch: PackedBatch) -> None:
     go = batch.host_group_off
@@ -148,6 +165,7 @@ def _reuse_channel(batch: PackedBatch, name: str) -> torch.Tensor:
 
 
 # ---- stage functions ------------------------------------------------------------------------
+@_on_batch_device(1)
 def fn_group_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
     """GPU fn_group_advantage (functions.hpp:143-161): f64, bit-identical; writes channel 'advantage'."""
     _require_rollouts(batch)
@@ -159,6 +177,7 @@ def fn_group_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) ->
     batch.channels["advantage"] = adv
 
 
+@_on_batch_device(1)
 def fn_ppo_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
     """GPU fn_ppo_advantage (functions.hpp:163-172): advantage = reward - value."""
     _require_rollouts(batch)
@@ -170,6 +189,7 @@ def fn_ppo_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
     batch.channels["advantage"] = adv
 
 
+@_on_batch_device(0)
 def broadcast_advantage(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
     """Per-token advantage stream adv_tok[t] = mask[t] ? f32(advantage[s]) : 0."""
     adv = _channel(batch, "advantage")
@@ -182,6 +202,7 @@ def broadcast_advantage(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
     return out
 
 
+@_on_batch_device(1)
 def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> None:
     """GAE reverse scan (new func tag 'gae_advantage'): token streams 'advantage', 'returns' + whitening sums."""
     _require_rollouts(batch)
@@ -202,6 +223,7 @@ def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
     batch.channels["_whiten_sums"] = wsum
 
 
+@_on_batch_device(0)
 def ppo_loss(batch: PackedBatch, ctx: StageContext, adv_source: str | None = None, loss_group_off=None,
              adv_tok_out: bool = False, events=None) -> dict:
     """Fused advantage + clipped surrogate + KL + masked aggregation. Returns device tensors.
@@ -267,6 +289,9 @@ def ppo_loss_sources(sources: list, ctx: StageContext, loss_group_off=None, adv_
     if cfg.whiten or cfg.want_grad:
         raise errors.Error("ppo_loss_sources: whitening / dlogp are single-source features")
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index != torch.cuda.current_device():  # launch on the consumer device (see _on_batch_device)
+        with torch.cuda.device(dev):
+            return ppo_loss_sources(sources, ctx, loss_group_off, adv_tok_out, events, dev)
     ng = 1 if loss_group_off is None else len(loss_group_off) - 1
     out = torch.empty(ng * 7, dtype=torch.float64, device=dev)
     arr = (_abi.LossSrc * len(sources))()
@@ -309,6 +334,7 @@ def ppo_loss_sources(sources: list, ctx: StageContext, loss_group_off=None, adv_
     return res
 
 
+@_on_batch_device(0)
 def reward_stats(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
     """detail::record_reward_stats (worker.hpp:177-190) on the device: f64 {count, sum, sum of squares} of the
     rollouts' 'reward' channel."""

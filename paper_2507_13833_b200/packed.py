@@ -110,9 +110,10 @@ class PackedBatch:
             b.streams[name] = torch.zeros(n, dtype=TOKEN_STREAMS[name], device=b.device)
         g = lambda k: _ptr(b.streams.get(k))  # noqa: E731
         st = stream if stream is not None else torch.cuda.current_stream(b.device).cuda_stream
-        _abi.check(_abi.lib().dfx_synth_tokens(seed, _ptr(b.ids), n_records, n_roll, _ptr(b.cu_seqlens), b.token_base,
-                                               b.token_span, g("lp"), g("old_lp"), g("ref_lp"), g("value_tok"),
-                                               g("token_reward"), g("mask"), g("token_id"), st))
+        with torch.cuda.device(b.device):  # libdfx launches on the current device
+            _abi.check(_abi.lib().dfx_synth_tokens(seed, _ptr(b.ids), n_records, n_roll, _ptr(b.cu_seqlens),
+                                                   b.token_base, b.token_span, g("lp"), g("old_lp"), g("ref_lp"),
+                                                   g("value_tok"), g("token_reward"), g("mask"), g("token_id"), st))
         return b
 
     # ---- ABI view ------------------------------------------------------------------------

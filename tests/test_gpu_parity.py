@@ -304,3 +304,25 @@ def test_reward_stats(O, dfx, case):
         q += r * r
     assert got[0] == len(sb.reward)
     assert abs(got[1] - s) <= 1e-12 * abs(s) and abs(got[2] - q) <= 1e-12 * abs(q)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_batch_on_non_current_device(dfx):
+    """The entry points launch on their stream's device: a batch on cuda:1 processed while cuda:0 is current gives
+    the same bytes as the same batch on cuda:0 (one process driving several GPUs)."""
+    torch.cuda.set_device(0)
+    outs = []
+    for dev in ("cuda:0", "cuda:1"):
+        b = dfx.PackedBatch.synthetic(7, 64, 4, dfx.TokenDist("uniform", 0, 1, 900), device=dev,
+                                      streams=("lp", "old_lp", "ref_lp", "mask", "token_reward", "value_tok"))
+        ctx = dfx.StageContext()
+        dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
+        dfx.fn_gae_advantage(dfx.NodeSpec("g"), b, ctx)
+        res = dfx.ppo_loss(b, ctx, adv_source="token")
+        assert torch.cuda.current_device() == 0
+        outs.append((b.channels["advantage"].cpu().numpy(), b.streams["advantage"][:b.token_span].cpu().numpy(),
+                     res["out"].cpu().numpy()))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()  # group advantage: bit-exact
+    # GAE's look-back may combine a different set of predecessor tiles run to run (f64 rounding), hence a tolerance
+    np.testing.assert_allclose(outs[1][1], outs[0][1], rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-6, atol=1e-9)

@@ -20,10 +20,8 @@ torch.cuda.set_device(0)
 loc = dfx.PackedBatch.synthetic(1, 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096), device="cuda:0")
 ctx = dfx.StageContext()
 dfx.fn_group_advantage(dfx.NodeSpec("a"), loc, ctx)
-with torch.cuda.device(1):  # libdfx launches on the thread's current device
-    rem = dfx.PackedBatch.synthetic(1, 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096), device="cuda:1",
-                                    first_id=1024)
-    dfx.fn_group_advantage(dfx.NodeSpec("a"), rem, dfx.StageContext())
+rem = dfx.PackedBatch.synthetic(1, 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096), device="cuda:1", first_id=1024)
+dfx.fn_group_advantage(dfx.NodeSpec("a"), rem, dfx.StageContext())  # launches on cuda:1 (the stream's device)
 torch.cuda.synchronize(1)
 rc = cudart.cudaDeviceEnablePeerAccess(1, 0)  # from cuda:0 (current) to cuda:1
 assert rc in (0, 704), rc                      # 704: already enabled
