@@ -78,7 +78,8 @@ dfx_status placement(uint32_t B, uint32_t W, uint32_t dp_p, uint32_t tp_p, uint3
 }  // namespace
 
 // ---- metadata pack / unpack --------------------------------------------------------------
-// One CTA per segment; the segment table travels by value in the kernel parameters (no H2D copy, no host sync).
+// Grid (segment, 256-entry chunk); the segment table travels by value in the kernel parameters (no H2D copy, no
+// host sync).
 // Unpack rebases: dst_go[dr+i] = go[i]-go[0]+droll ; dst_cu[droll+j] = cu[j]-cu[0]+dtok ;
 // roll_group[droll+j] = dr + (record of rollout j) ; ids / channels copied. Source pointers may be peer-mapped
 // (NVLink pull transport): the kernel then reads the producer GPU's metadata directly.
@@ -91,10 +92,15 @@ struct SegBatch {
 
 __global__ void unpack_kernel(const SegBatch sb, int n_ch, uint64_t* dst_ids, int32_t* dst_go, int32_t* dst_rg,
                               int64_t* dst_cu) {
+  // CTA (segment x, chunk y) handles records and rollouts [y*B, y*B + B): the source metadata often sits in a
+  // peer GPU's memory, so the loads of a segment are spread over many CTAs instead of looping in one (each loop
+  // trip would pay an NVLink round trip)
   const dfx_seg_meta& m = sb.seg[blockIdx.x];
   double* const* dst_ch = sb.dst_ch;
+  const int64_t i = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (i > m.n_rec && i > m.n_roll) return;
   const int64_t g0 = m.group_off[0], c0 = m.cu[0];
-  for (int64_t i = threadIdx.x; i <= m.n_rec; i += blockDim.x) {
+  if (i <= m.n_rec) {
     const int64_t gi = m.group_off[i];
     dst_go[m.dst_rec + i] = (int32_t)(gi - g0 + m.dst_roll);
     if (i < m.n_rec) {
@@ -103,30 +109,30 @@ __global__ void unpack_kernel(const SegBatch sb, int n_ch, uint64_t* dst_ids, in
       for (int64_t j = gi; j < ge; ++j) dst_rg[m.dst_roll + (j - g0)] = (int32_t)(m.dst_rec + i);
     }
   }
-  for (int64_t j = threadIdx.x; j <= m.n_roll; j += blockDim.x) {
-    dst_cu[m.dst_roll + j] = m.cu[j] - c0 + m.dst_tok;
-    if (j < m.n_roll)
-      for (int c = 0; c < n_ch; ++c) dst_ch[c][m.dst_roll + j] = m.ch[c][j];
+  if (i <= m.n_roll) {
+    dst_cu[m.dst_roll + i] = m.cu[i] - c0 + m.dst_tok;
+    if (i < m.n_roll)
+      for (int c = 0; c < n_ch; ++c) dst_ch[c][m.dst_roll + i] = m.ch[c][i];
   }
 }
 
-// Pack: gather one segment's metadata into a contiguous buffer laid out as
-//   ids u64[n_rec] | cu i64[n_roll+1] | ch f64[n_ch][n_roll] | group_off i32[n_rec+1]
 __global__ void pack_kernel(const SegBatch sb, int n_ch) {
   const dfx_seg_meta& m = sb.seg[blockIdx.x];
+  const int64_t i = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;  // chunked like unpack_kernel
+  if (i > m.n_rec && i > m.n_roll) return;
   uint8_t* o = sb.out[blockIdx.x];
   uint64_t* ids = reinterpret_cast<uint64_t*>(o);
   int64_t* cu = reinterpret_cast<int64_t*>(ids + m.n_rec);
   double* ch = reinterpret_cast<double*>(cu + m.n_roll + 1);
   int32_t* go = reinterpret_cast<int32_t*>(ch + int64_t(n_ch) * m.n_roll);
-  for (int64_t i = threadIdx.x; i <= m.n_rec; i += blockDim.x) {
+  if (i <= m.n_rec) {
     go[i] = m.group_off[i];
     if (i < m.n_rec) ids[i] = m.ids[i];
   }
-  for (int64_t j = threadIdx.x; j <= m.n_roll; j += blockDim.x) {
-    cu[j] = m.cu[j];
-    if (j < m.n_roll)
-      for (int c = 0; c < n_ch; ++c) ch[int64_t(c) * m.n_roll + j] = m.ch[c][j];
+  if (i <= m.n_roll) {
+    cu[i] = m.cu[i];
+    if (i < m.n_roll)
+      for (int c = 0; c < n_ch; ++c) ch[int64_t(c) * m.n_roll + i] = m.ch[c][i];
   }
 }
 
@@ -185,9 +191,14 @@ dfx_status dfx_reshard_unpack(const dfx_seg_meta* segs, int32_t n_segs, int32_t 
   for (int32_t s0 = 0; s0 < n_segs; s0 += kSegsPerLaunch) {
     const int32_t n = std::min<int32_t>(kSegsPerLaunch, n_segs - s0);
     SegBatch sb{};
-    for (int32_t i = 0; i < n; ++i) sb.seg[i] = segs[s0 + i];
+    int64_t span = 1;
+    for (int32_t i = 0; i < n; ++i) {
+      sb.seg[i] = segs[s0 + i];
+      span = std::max<int64_t>(span, std::max(segs[s0 + i].n_rec, segs[s0 + i].n_roll) + 1);
+    }
     for (int32_t c = 0; c < n_ch; ++c) sb.dst_ch[c] = dst_ch[c];
-    unpack_kernel<<<n, 256, 0, stream>>>(sb, n_ch, dst_ids, dst_group_off, dst_roll_group, dst_cu);
+    unpack_kernel<<<dim3(n, unsigned((span + 255) / 256)), 256, 0, stream>>>(sb, n_ch, dst_ids, dst_group_off,
+                                                                           dst_roll_group, dst_cu);
     DFX_LAUNCH_CHECK("unpack_kernel");
   }
   return DFX_OK;
@@ -200,11 +211,13 @@ dfx_status dfx_reshard_pack(const dfx_seg_meta* segs, int32_t n_segs, int32_t n_
   for (int32_t s0 = 0; s0 < n_segs; s0 += kSegsPerLaunch) {
     const int32_t n = std::min<int32_t>(kSegsPerLaunch, n_segs - s0);
     SegBatch sb{};
+    int64_t span = 1;
     for (int32_t i = 0; i < n; ++i) {
       sb.seg[i] = segs[s0 + i];
       sb.out[i] = out[s0 + i];
+      span = std::max<int64_t>(span, std::max(segs[s0 + i].n_rec, segs[s0 + i].n_roll) + 1);
     }
-    pack_kernel<<<n, 256, 0, stream>>>(sb, n_ch);
+    pack_kernel<<<dim3(n, unsigned((span + 255) / 256)), 256, 0, stream>>>(sb, n_ch);
     DFX_LAUNCH_CHECK("pack_kernel");
   }
   return DFX_OK;
