@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--materialize", action="store_true",
                     help="copy remote records into a local consumer batch before the loss (default: the loss kernel "
                          "reads them in place over NVLink)")
+    ap.add_argument("--tp-read", action="store_true",
+                    help="TP partners on different GPUs: every TP worker streams its whole group (the partner's half "
+                         "over NVLink) instead of the default TP-split loss")
     ap.add_argument("--placement", default="box", choices=["box", "store"],
                     help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
                          "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")
@@ -159,7 +162,7 @@ class DagSlice:
     STAGE = "group_advantage_compute"
 
     def __init__(self, dfx, world, rank, records, ctx, Layout, Topology, Store, StagePlan, placement="box", workers=8,
-                 lazy=True, dev=None):
+                 lazy=True, dev=None, tp_split=True):
         self.dfx, self.ctx, self.it = dfx, ctx, 0
         self.lazy, self.dev = lazy, dev
         self.placement = placement
@@ -181,6 +184,17 @@ class DagSlice:
         from paper_2507_13833_b200.reshard import Plan
         self.cross = Plan(self.topo, self.prod, self.cons, [self.per] * self.prod.dp, rank).cross
         self.last = None
+        # TP-split loss (one worker per GPU, TP partners on different GPUs): each TP worker streams only the
+        # rollouts it holds and the pair folds its 56-byte loss rows (all-gather + dfx_loss_combine) -- instead of
+        # both TP workers streaming the whole group, the partner's half over NVLink (--tp-read)
+        self.tp_group = None
+        if tp_split and lazy and self.cross and placement == "box" and workers == world:
+            import torch.distributed as dist
+            for d in range(self.cons.dp):
+                ranks = sorted({self.topo.gpu_of_worker[w] for w in range(workers) if self.cons.dp_rank(w) == d})
+                g = dist.new_group(ranks=ranks)  # every rank creates every group, same order
+                if rank in ranks:
+                    self.tp_group = g
 
     def step(self, batch, events=None):
         dfx, ctx = self.dfx, self.ctx
@@ -188,7 +202,13 @@ class DagSlice:
         for j, p in enumerate(self.local_p):
             self.store.put(self.STAGE, self.it, p, 0, batch.view_records(j * self.per, (j + 1) * self.per))
         cb = self.store.ensure_ready(self.STAGE, self.it, self.cons, lazy=self.lazy)
-        if cb.sources is not None:  # TP partner's records read in place over NVLink by the loss kernel
+        if cb.sources is not None and self.tp_group is not None:  # TP-split: this GPU's rollouts, then fold
+            from paper_2507_13833_b200.packed import PackedBatch
+            mine = [x for grp in cb.sources for x in grp if isinstance(x, PackedBatch)]
+            assert len(mine) == 1, "TP-split expects one local producer group per GPU"
+            res = dfx.ppo_loss(mine[0], ctx, adv_source="rollout", adv_tok_out=True, events=events)
+            res["out"] = dfx.tp_combine_loss(res["out"], ctx, self.tp_group)
+        elif cb.sources is not None:  # TP partner's records read in place over NVLink by the loss kernel
             srcs = [x for grp in cb.sources for x in grp]
             res = dfx.ppo_loss_sources(srcs, ctx, loss_group_off=cb.roll_off, adv_tok_out=True, events=events,
                                        device=self.dev)
@@ -205,14 +225,15 @@ class DagSlice:
         """The partner-GPU runs the last step's loss read over NVLink (lazy exchange), else []."""
         from paper_2507_13833_b200.reshard import RemoteSource
         cb = self.last
-        if cb is None or cb.sources is None:
+        if cb is None or cb.sources is None or self.tp_group is not None:
             return []
         return [x for grp in cb.sources for x in grp if isinstance(x, RemoteSource)]
 
     def launches_per_step(self):
         # grpo_adv + loss_slots + finalize; records crossing GPUs: + the materializing unpack kernel (lazy: none,
         # the loss kernel reads the partner's records over NVLink)
-        return 3 + (1 if self.cross and not self.lazy else 0)
+        # (TP-split: + dfx_loss_combine after the 56-byte all-gather)
+        return 3 + (1 if self.cross and (not self.lazy or self.tp_group is not None) else 0)
 
     def describe(self):
         if not self.cross:
@@ -220,6 +241,10 @@ class DagSlice:
         elif self.lazy and self.placement == "store":
             mode = ("records cross GPUs (dense slice/exchange/concat): each consumer maps the remote slices (CUDA "
                     "IPC) and the loss kernel streams them over NVLink in place (dfx_ppo_loss_multi), no copy")
+        elif self.lazy and self.tp_group is not None:
+            mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC, the "
+                    "consumer's view of the group); TP-split loss: each TP worker streams the rollouts it holds and "
+                    "the pair folds its loss rows (56 B all-gather + dfx_loss_combine), no token crosses NVLink")
         elif self.lazy:
             mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC) and the "
                     "loss kernel streams it over NVLink in place (dfx_ppo_loss_multi), no copy")
@@ -268,7 +293,7 @@ def run_dfx(args):
     ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
     stream = torch.cuda.current_stream(dev)
     resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement,
-                    args.workers, lazy=not args.materialize, dev=dev)
+                    args.workers, lazy=not args.materialize, dev=dev, tp_split=not args.tp_read)
 
     ev0, ev1 = C.c_void_p(), C.c_void_p()
     _abi.check(L.dfx_event_create(C.byref(ev0)))
@@ -293,9 +318,11 @@ def run_dfx(args):
     torch.cuda.synchronize()
 
     # the steady-state step is launch-bound at this size: capture it once in a CUDA graph when the
-    # reshard has no host synchronization (all N <= 4 box placements)
+    # reshard has no host synchronization (box placements with zero-copy views, and the lazy TP-split step whose
+    # device work is the adv kernel, two NCCL barriers, the loss kernel, a 56-byte all-gather and the fold); the
+    # store's host bookkeeping (put / ensure_ready on a template hit) is identical every step and stays outside
     graph = None
-    if not resh.cross and not args.no_graph:
+    if (not resh.cross or resh.tp_group is not None) and not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step()
@@ -380,6 +407,14 @@ def run_dfx(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if graph is not None and resh.cross:
+            # the graph holds captured NCCL work of the TP / barrier communicators: tearing those down under the
+            # ProcessGroupNCCL watchdog can hang; every collective of the run has completed here, so leave without
+            # the teardown
+            torch.cuda.synchronize()
+            sys.stdout.flush()
+            sys.stderr.flush()
+            os._exit(0)
         dist.destroy_process_group()
 
 

@@ -197,6 +197,16 @@ size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_sr
 dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
                               const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream);
 
+/* TP-split loss: when a consumer group's records sit on several GPUs (its TP
+ * workers' producers), each TP rank runs the loss over the rollouts it holds
+ * and the ranks exchange their dfx_loss_out rows (an all-gather of 56 B per
+ * group); this folds parts[n_parts][n_groups] (device, rank order) into the
+ * group results, re-weighting each mean by its denominator. Every rank gets
+ * the same bits. Token-mean / sequence-mean aggregations (no whitening/dlogp,
+ * which need group-wide statistics before the streaming pass). */
+dfx_status dfx_loss_combine(const dfx_loss_out* parts, int32_t n_parts, int32_t n_groups, const dfx_loss_cfg* cfg,
+                            dfx_loss_out* out, dfx_stream stream);
+
 /* Per-iteration reward statistics, replacing detail::record_reward_stats
  * (worker.hpp:177-190): out[0..3) = {count, sum, sum of squares} of the
  * rollouts' "reward" channel (device f64), so the cluster reduction of

@@ -78,6 +78,7 @@ def _declare(L):
     L.dfx_ppo_loss_multi_workspace_bytes.argtypes = [C.POINTER(LossSrc), i32, i32]
     L.dfx_ppo_loss_multi.argtypes = [C.POINTER(LossSrc), i32, C.POINTER(LossCfg), C.POINTER(LossArgs), P, sz, P]
     L.dfx_reward_stats.argtypes = [C.POINTER(Packed), P, P]
+    L.dfx_loss_combine.argtypes = [P, i32, i32, C.POINTER(LossCfg), P, P]
     L.dfx_check_flags.argtypes = [P, P]
     L.dfx_synth_tokens.argtypes = [u64, P, i64, i32, P, i64, i64, P, P, P, P, P, P, P, P]
     L.dfx_event_create.argtypes = [C.POINTER(P)]
@@ -98,7 +99,9 @@ EXPORTS = ("dfx_last_error", "dfx_version", "dfx_grpo_advantage", "dfx_broadcast
            "dfx_gae_workspace_bytes", "dfx_gae", "dfx_ppo_loss_workspace_bytes", "dfx_ppo_loss",
            "dfx_ppo_loss_multi_workspace_bytes", "dfx_ppo_loss_multi", "dfx_check_flags",
            "dfx_synth_tokens", "dfx_serialize_plan", "dfx_serialize_records",
-           "dfx_blob_index", "dfx_blob_unpack", "dfx_reward_stats", "dfx_copy_batch", "dfx_copy_sm", "dfx_view_meta", "dfx_copy_many", "dfx_event_create", "dfx_event_destroy", "dfx_event_record", "dfx_event_elapsed_ms")
+           "dfx_blob_index", "dfx_blob_unpack", "dfx_reward_stats", "dfx_loss_combine", "dfx_copy_batch",
+           "dfx_copy_sm", "dfx_view_meta", "dfx_copy_many", "dfx_event_create", "dfx_event_destroy",
+           "dfx_event_record", "dfx_event_elapsed_ms")
 
 
 def check(status: int) -> None:

@@ -600,6 +600,35 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
   }
 }
 
+// Merge per-part results of one loss group (the TP-split loss: each TP rank reduced the rollouts it holds):
+// the means are re-weighted by their denominators, parts folded in index order (every rank gets the same bits).
+__global__ void loss_combine_kernel(const dfx_loss_out* parts, int n_parts, int n_groups, int agg, double beta,
+                                    dfx_loss_out* out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  double pg = 0, kl = 0, clip = 0, akl = 0, N = 0, S = 0;
+  for (int k = 0; k < n_parts; ++k) {
+    const dfx_loss_out p = parts[(int64_t)k * n_groups + g];
+    const double den = agg == DFX_AGG_TOKEN_MEAN ? p.n_tokens : p.n_seqs;
+    pg += p.pg_loss * den;
+    kl += p.kl * den;
+    clip += p.clipfrac * p.n_tokens;
+    akl += p.approx_kl * p.n_tokens;
+    N += p.n_tokens;
+    S += p.n_seqs;
+  }
+  const double den = agg == DFX_AGG_TOKEN_MEAN ? N : S;
+  dfx_loss_out o;
+  o.pg_loss = den > 0 ? pg / den : 0.0;
+  o.kl = den > 0 ? kl / den : 0.0;
+  o.loss = o.pg_loss + beta * o.kl;
+  o.clipfrac = N > 0 ? clip / N : 0.0;
+  o.approx_kl = N > 0 ? akl / N : 0.0;
+  o.n_tokens = N;
+  o.n_seqs = S;
+  out[g] = o;
+}
+
 }  // namespace dfx
 
 using namespace dfx;
@@ -921,6 +950,16 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
 dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
                               const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
   return ppo_loss_impl(srcs, n_src, cfg, args, workspace, ws_bytes, stream);
+}
+
+dfx_status dfx_loss_combine(const dfx_loss_out* parts, int32_t n_parts, int32_t n_groups, const dfx_loss_cfg* cfg,
+                            dfx_loss_out* out, dfx_stream stream) {
+  if (n_groups <= 0) return DFX_OK;
+  if (!parts || !out || !cfg || n_parts <= 0)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_loss_combine: bad argument");
+  loss_combine_kernel<<<(n_groups + 127) / 128, 128, 0, stream>>>(parts, n_parts, n_groups, cfg->agg, cfg->beta, out);
+  DFX_LAUNCH_CHECK("loss_combine_kernel");
+  return DFX_OK;
 }
 
 dfx_status dfx_check_flags(const int32_t* flags, dfx_stream stream) {

@@ -334,6 +334,29 @@ def ppo_loss_sources(sources: list, ctx: StageContext, loss_group_off=None, adv_
     return res
 
 
+def tp_combine_loss(out: torch.Tensor, ctx: StageContext, group) -> torch.Tensor:
+    """TP-split loss: `out` [n_groups, 7] is this rank's loss over the rollouts of each group it holds (ppo_loss /
+    ppo_loss_sources); the ranks of `group` (the TP workers of those consumer groups, one process per GPU)
+    all-gather their rows (56 B per group over NCCL) and fold them with dfx_loss_combine, so every TP worker ends
+    with the group's loss over all its rollouts while each GPU streamed only the tokens it holds -- instead of
+    every TP worker streaming the whole group (the partner's half over NVLink)."""
+    import torch.distributed as dist
+    cfg = ctx.loss
+    if cfg.whiten or cfg.want_grad:
+        raise errors.Error("tp_combine_loss: whitening / dlogp need group-wide statistics before the loss pass")
+    ng = out.shape[0]
+    n = dist.get_world_size(group)
+    parts = torch.empty(n * ng * 7, dtype=torch.float64, device=out.device)
+    dist.all_gather_into_tensor(parts, out.reshape(-1).contiguous(), group=group)
+    res = torch.empty(ng * 7, dtype=torch.float64, device=out.device)
+    c = _abi.LossCfg(cfg.clip_low, cfg.clip_high, cfg.beta, float(ctx.advantage_eps), _abi.KL[cfg.kl],
+                     _abi.AGG[cfg.agg], _abi.ADV["rollout"], 0)
+    with torch.cuda.device(out.device):
+        _abi.check(_abi.lib().dfx_loss_combine(_ptr(parts), n, ng, C.byref(c), _ptr(res),
+                                               ctx.cuda_stream(out.device)))
+    return res.view(ng, 7)
+
+
 @_on_batch_device(0)
 def reward_stats(batch: PackedBatch, ctx: StageContext) -> torch.Tensor:
     """detail::record_reward_stats (worker.hpp:177-190) on the device: f64 {count, sum, sum of squares} of the

@@ -3,7 +3,8 @@
 Box placement with W = 2 logical workers on 2 GPUs: producer dp 2 (tp 1), consumer dp 1 (tp 2), so the one
 consumer group's TP workers sit on different GPUs and each GPU needs its partner's producer group. The lazy path
 maps the partner's batch (CUDA IPC) and the loss kernel reads it over NVLink in place; the reference path pulls it
-into a local consumer batch first. Losses must agree to f32 partial-sum rounding (the slot windows differ), per-token
+into a local consumer batch first; the TP-split path streams only the local group and folds the two loss rows
+(all-gather + dfx_loss_combine). Losses must agree to f32 partial-sum rounding (the slot windows differ), per-token
 advantages bit-exactly.
 """
 import os
@@ -42,6 +43,14 @@ for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("unif
     assert [isinstance(x, RemoteSource) for x in srcs] == [rank == 1, rank == 0], srcs
     res = dfx.ppo_loss_sources(srcs, ctx, loss_group_off=cb.roll_off, adv_tok_out=True, device=dev)
     got = res["out"].cpu().numpy()[0]
+    # TP-split: each GPU streams only its own producer group, the pair folds the loss rows (all-gather + combine)
+    mine = [x for x in srcs if isinstance(x, dfx.PackedBatch)]
+    part = dfx.ppo_loss(mine[0], ctx, adv_source="rollout")["out"]
+    split = dfx.tp_combine_loss(part, ctx, None)
+    both = [torch.empty_like(split) for _ in range(world)]
+    dist.all_gather(both, split)
+    assert all(b_.cpu().numpy().tobytes() == split.cpu().numpy().tobytes() for b_ in both)  # same bits everywhere
+    split = split.cpu().numpy()[0]
     lazy_store.worker_done(it)
     rb = ref_store.ensure_ready("s", it, Layout(1, 2))
     ref = dfx.ppo_loss(rb.batch, dfx.StageContext(), adv_source="rollout", adv_tok_out=True)
@@ -49,6 +58,8 @@ for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("unif
     assert got[5] == want[5] and got[6] == want[6], (got, want)  # token / sequence counts exact
     # f32 partial sums over different slot windows (each source keeps its own token coordinates): f32 rounding
     np.testing.assert_allclose(got[:5], want[:5], rtol=2e-6, atol=1e-9)
+    assert split[5] == want[5] and split[6] == want[6], (split, want)
+    np.testing.assert_allclose(split[:5], want[:5], rtol=2e-6, atol=1e-9)
     # per-token advantages: source k's tokens land at the consumer's cumulative token offset
     want_tok = ref["adv_tok"].cpu().numpy()
     off = 0

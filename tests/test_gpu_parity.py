@@ -326,3 +326,26 @@ def test_batch_on_non_current_device(dfx):
     # GAE's look-back may combine a different set of predecessor tiles run to run (f64 rounding), hence a tolerance
     np.testing.assert_allclose(outs[1][1], outs[0][1], rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("agg", ["token-mean", "seq-mean-token-sum", "seq-mean-token-mean"])
+def test_loss_combine_parts(dfx, agg):
+    """dfx_loss_combine (the TP-split loss): the loss rows of disjoint record ranges fold into the whole batch's."""
+    from paper_2507_13833_b200 import _abi
+    from paper_2507_13833_b200.packed import _ptr
+    b = dfx.PackedBatch.synthetic(9, 96, 4, dfx.TokenDist("skewed", 0, 1, 3000), device="cuda")
+    ctx = dfx.StageContext()
+    ctx.loss = dfx.LossConfig(agg=agg)
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
+    whole = dfx.ppo_loss(b, ctx, adv_source="rollout")["out"].cpu().numpy()[0]
+    cuts = [0, 17, 60, 96]
+    parts = torch.cat([dfx.ppo_loss(b.view_records(cuts[i], cuts[i + 1]), ctx, adv_source="rollout")["out"]
+                       for i in range(3)]).reshape(-1)
+    out = torch.empty(7, dtype=torch.float64, device="cuda")
+    c = _abi.LossCfg(ctx.loss.clip_low, ctx.loss.clip_high, ctx.loss.beta, float(ctx.advantage_eps), _abi.KL[ctx.loss.kl], _abi.AGG[agg],
+                     _abi.ADV["rollout"], 0)
+    _abi.check(_abi.lib().dfx_loss_combine(_ptr(parts), 3, 1, C.byref(c), _ptr(out),
+                                           torch.cuda.current_stream().cuda_stream))
+    got = out.cpu().numpy()
+    assert got[5] == whole[5] and got[6] == whole[6]
+    np.testing.assert_allclose(got[:5], whole[:5], rtol=2e-6, atol=1e-9)
