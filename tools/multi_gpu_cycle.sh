@@ -9,9 +9,9 @@ timeout 600 python -m pytest tests/test_reshard.py -q -x -m gpu -p no:cacheprovi
 run() {  # name N extra...
   local name=$1 n=$2; shift 2
   if [ "$n" = 1 ]; then
-    timeout 600 python bench.py --steps 50 "$@" > gpurun_out/multi_${TAG}_${name}.log 2>&1
+    timeout 300 python bench.py --steps 50 "$@" > gpurun_out/multi_${TAG}_${name}.log 2>&1
   else
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+    timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
       --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --steps 50 "$@" > gpurun_out/multi_${TAG}_${name}.log 2>&1
   fi
   grep '^{' gpurun_out/multi_${TAG}_${name}.log | tail -1 > gpurun_out/multi_${TAG}_${name}.json
@@ -32,6 +32,7 @@ run n2 2
 run n4 4
 run n4_w4 4 --workers 4
 run n2_w2 2 --workers 2
+run n4_w4_read 4 --workers 4 --tp-read
 run n4_store 4 --placement store
 run c4_n1 1 --workload c4 --steps 20
 run c4_n2 2 --workload c4 --steps 20

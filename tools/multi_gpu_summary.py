@@ -40,9 +40,12 @@ if bs:
         raw.append(json.dumps(d))
 out += ["",
         "- n1/n2/n4: the default bench (C2 per GPU, box placement W=8): zero-copy reshard, near-linear.",
-        "- n2_w2 / n4_w4: the N=8 layout (one logical worker per GPU, TP partners on different GPUs) on 2 / 4 GPUs:",
-        "  the partner's group crosses NVLink every step; the loss kernel reads it in place at ~73 % of the",
-        "  770 GB/s peer-copy rate. Projected N=8 default: ~0.82 ms/step, ~325 G tokens/s.",
+        "- n2_w2 / n4_w4: the N=8 layout (one logical worker per GPU, TP partners on different GPUs) on 2 / 4 GPUs,",
+        "  TP-split loss (default): each TP worker streams the rollouts it holds, the pair folds 56-byte loss rows",
+        "  (NCCL all-gather + dfx_loss_combine), step captured in a CUDA graph. Projected N=8: ~0.15 ms/step, ~1.8 T",
+        "  tokens/s.",
+        "- n4_w4_read (--tp-read): the same layout with every TP worker streaming its whole group, the partner's",
+        "  half read in place over NVLink by the multi-source loss kernel at ~73 % of the 770 GB/s peer-copy rate.",
         "- n4_store: one DataBuffer per GPU (dense slice/exchange/concat), consumers read remote slices in place.",
         "- c4_*: BASELINE config 4, the materialized DataBuffer round trip dp8 -> dp4 -> dp8 (16.8M tokens, strong",
         "  scaling), host-orchestration bound.",
