@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   unsigned int epoch;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(epoch) : "l"(p.ticket + 2) : "memory");
   const unsigned int F_AGG = (epoch << 2) | 1u, F_INC = (epoch << 2) | 2u;
-  const float gam = (float)p.gamma, glf = (float)p.gl;
+  // f64 deltas and maps: with lambda = 1 the f32 rounding of each delta (~eps |V|) does not telescope and
+  // would dominate returns that are small against the values
+  const double gamd = p.gamma, gld = p.gl;
   __syncthreads();  // s_bar initialised, next-token slot written
   mbar_wait(&s_bar, 0);
 
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   // (ident) and never stored.
   const int s0 = lane & 7;
   const float vn_cross = s_v[tid * 32 + 32];  // first V of the next thread (or the token after the tile)
-  float Hd = 0.0f, Hc = 1.0f, Td = 0.0f, Tc = 1.0f;
+  double Hd = 0.0, Hc = 1.0, Td = 0.0, Tc = 1.0;  // the thread's 32-token map, f64
   uint32_t link = 0u, mbits = 0u;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -216,30 +218,30 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
     const uint32_t mnx = s_m[i0 + 4] ? 1u : 0u;
     const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
-    float fd = 0.0f, fc = 1.0f;
+    double fd = 0.0, fc = 1.0;
 #pragma unroll
     for (int k = 3; k >= 0; --k) {
       const int q = ch * 4 + k;
       const uint32_t mnext = k == 3 ? mnx : (((m4 >> (8 * (k + 1))) & 0xffu) ? 1u : 0u);
       const bool lk = mnext && !((last >> q) & 1u);
       const float vnext = k == 3 ? vnx : vv[k + 1];
-      const float dq = (lk ? fmaf(gam, vnext, rr[k]) : rr[k]) - vv[k];
+      const double dq = (lk ? fma(gamd, (double)vnext, (double)rr[k]) : (double)rr[k]) - (double)vv[k];
       if (!((ident >> q) & 1u)) {
-        fd = lk ? fmaf(glf, fd, dq) : dq;
-        fc = lk ? fc * glf : 0.0f;
+        fd = lk ? fma(gld, fd, dq) : dq;
+        fc = lk ? fc * gld : 0.0;
       }
       link |= (lk ? 1u : 0u) << q;
       mbits |= (((m4 >> (8 * k)) & 0xffu) ? 1u : 0u) << q;
     }
     if (ch >= s0) {  // append on the right: F o C
-      Td = fmaf(Tc, fd, Td);
+      Td = fma(Tc, fd, Td);
       Tc *= fc;
     } else {
-      Hd = fmaf(Hc, fd, Hd);
+      Hd = fma(Hc, fd, Hd);
       Hc *= fc;
     }
   }
-  Aff S{(double)fmaf(Hc, Td, Hd), (double)(Hc * Tc)};
+  Aff S{fma(Hc, Td, Hd), Hc * Tc};
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double od = __shfl_down_sync(kFull, S.d, o), oc = __shfl_down_sync(kFull, S.c, o);
@@ -268,8 +270,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   // pass 2 in descending cyclic order from chunk s-1: chunks s-1 .. 0 start from the carry tail(X_in), chunks
   // 7 .. s from X_in. Interior tiles write A over r at once and R over V one chunk late, after the chunk below
   // has read this chunk's first V as its successor value.
-  const float Xin = (float)fma(E.c, Xd, E.d);
-  float X = fmaf(Tc, Xin, Td);
+  // the per-token recurrence runs in f64 from the carry: A_t = delta_t + gl A_{t+1} keeps the oracle's accuracy
+  // where long discounted sums cancel (values stored as f32 once)
+  const double Xin = fma(E.c, Xd, E.d);
+  double X = fma(Tc, Xin, Td);
   float wa = 0.0f, wa2 = 0.0f;
   float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
   int pend_i = -1;
@@ -289,15 +293,15 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
       const int q = ch * 4 + k;
       const bool lk = (link >> q) & 1u;
       const float vnext = k == 3 ? vnx : vv[k + 1];
-      const float dq = (lk ? fmaf(gam, vnext, rr[k]) : rr[k]) - vv[k];
-      const float A = lk ? fmaf(glf, X, dq) : dq;
+      const double dq = (lk ? fma(gamd, (double)vnext, (double)rr[k]) : (double)rr[k]) - (double)vv[k];
+      const double A = lk ? fma(gld, X, dq) : dq;
       X = ((ident >> q) & 1u) ? X : A;
-      oa[k] = X;
-      orr[k] = X + vv[k];
+      oa[k] = (float)X;
+      orr[k] = (float)(X + (double)vv[k]);
       if (WHITEN) {
         const float mw = ((mbits & ~ident) >> q) & 1u ? 1.0f : 0.0f;
-        wa = fmaf(mw, X, wa);
-        wa2 = fmaf(mw * X, X, wa2);
+        wa = fmaf(mw, oa[k], wa);
+        wa2 = fmaf(mw * oa[k], oa[k], wa2);
       }
     }
     if (interior) {
