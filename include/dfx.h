@@ -115,8 +115,8 @@ dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream s
  * whitening sums whiten[3] = {sum m*A, sum m*A^2, sum m} (device f64). */
 /* One reverse affine scan over the whole token line (the chain breaks at rollout
  * ends by itself): a prep kernel marks rollout ends in a token bitmap, a
- * single-pass decoupled look-back scan over 2048-token CTA tiles does the rest
- * (f32 inside a thread's chunk, f64 across chunks), and with whitening a
+ * single-pass decoupled look-back scan over 4096-token CTA tiles does the rest
+ * (f32 inputs/outputs, deltas and recurrences in f64), and with whitening a
  * finish kernel reduces the per-tile sums in tile order (deterministic).
  * Workspace (dfx_gae_workspace_bytes) must be zero-filled once at allocation;
  * the kernels keep it consistent across calls (epoch-tagged tile records, the

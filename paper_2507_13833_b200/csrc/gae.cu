@@ -22,7 +22,7 @@
 // Tile state is one 16-byte record per tile {f64 x ; f32 c ; u32 tag} written and polled with single relaxed
 // 128-bit accesses, so value and status are never seen out of order and no fence is needed (on sm_100 a gpu-scope
 // fence or acquire invalidates L1: CCTL.IVALL, measured as the top stall of a fenced version).
-// Arithmetic: f32 inside a thread's chunk of 4 tokens / 32 tokens, f64 across threads; outputs f32. HBM-bound:
+// Arithmetic: f32 inputs and outputs; deltas, chunk maps, scans and the per-token recurrence in f64. HBM-bound:
 // 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map. Design history: profiles/r01_gae_experiments.md.
 #include <algorithm>
 #include <cstdlib>
