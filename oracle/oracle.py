@@ -125,6 +125,7 @@ def _declare_ref(L):
     L.ref_hash_bytes.restype = None
     L.ref_generate.argtypes = [u64, C.c_int, u32, u32, u32, u32, u32, P, u32, P, P]
     L.ref_fill_channels.argtypes = [u64, P, u32, u32, P, P, P]
+    L.ref_loader_ids.argtypes = [u64, u32, u32, u64, C.c_int, u32, u64, P]
     L.ref_advantage.argtypes = [C.c_int, u32, P, P, P, f64, P]
     L.ref_serialize_packed.restype = i64
     L.ref_serialize_packed.argtypes = [u32, P, P, P, P, P, P, C.c_int, P, P, C.c_int, P, P, P, i64]
@@ -314,6 +315,14 @@ def serialize_packed(ids, group_off, tok_count, cu_seqlens, streams=(), channels
     n = lib().dfo_serialize_packed(*args, None)
     out = np.zeros(n, np.uint8)
     lib().dfo_serialize_packed(*args, ptr(out))
+    return out
+
+
+def ref_loader_ids(dataset_n, dp, dp_rank, seed, shuffle, iteration, global_batch):
+    """The reference DataLoader (make_group_loader(...).next_batch, distflow/data_plane.hpp:124-209) -> the batch's
+    sample ids; raises OracleError on the reference's errors."""
+    out = np.zeros(max(1, global_batch // max(dp, 1)), np.uint64)
+    _ref_check(ref().ref_loader_ids(dataset_n, dp, dp_rank, seed, int(shuffle), iteration, global_batch, ptr(out)))
     return out
 
 

@@ -153,6 +153,25 @@ int ref_generate(uint64_t seed, int kind, uint32_t value, uint32_t mn, uint32_t 
   }
 }
 
+// make_group_loader(synthetic dataset of dataset_n rows, dp, dp_rank, seed, shuffle).next_batch(iteration,
+// global_batch): writes the sample ids of the batch (global_batch / dp of them) into out_ids.
+int ref_loader_ids(uint64_t dataset_n, uint32_t dp, uint32_t dp_rank, uint64_t seed, int shuffle,
+                   uint32_t iteration, uint64_t global_batch, uint64_t* out_ids) {
+  try {
+    DatasetSpec spec;
+    spec.synthetic_n = dataset_n;
+    spec.prompt_tokens = 1;
+    ParallelLayout layout;
+    layout.dp_size = dp;
+    const DataLoader loader = make_group_loader(spec, layout, dp_rank, seed, shuffle != 0);
+    const auto recs = loader.next_batch(iteration, global_batch);
+    for (size_t i = 0; i < recs.size(); ++i) out_ids[i] = recs[i].sample_id;
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 // fn_reward / fn_value / fn_ref_logprob on records with n_roll empty rollouts.
 int ref_fill_channels(uint64_t seed, const uint64_t* ids, uint32_t n_records, uint32_t n_roll,
                       double* reward, double* value, double* ref_logprob) {

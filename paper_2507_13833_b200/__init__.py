@@ -14,6 +14,7 @@ from .functions import (FunctionRegistry, LossConfig, NodeSpec, StageContext, bu
                         ppo_loss, ppo_loss_sources, preset_dag, registry_bind, reward_stats, aggregate_metrics,
                         tp_combine_loss)
 from .packed import PackedBatch  # noqa: E402,F401
+from .loader import DataLoader, ShardRange, make_group_loader, shard_dataset  # noqa: E402,F401
 from .synth import TokenDist  # noqa: E402,F401
 from . import wire  # noqa: E402,F401
 

@@ -96,9 +96,15 @@ class PackedBatch:
 
     @staticmethod
     def synthetic(seed: int, n_records: int, n_roll: int, dist: synth.TokenDist, device="cuda", first_id: int = 0,
-                  streams=("lp", "old_lp", "ref_lp", "mask"), stream=None) -> "PackedBatch":
-        """Synthetic batch: lengths/channels on the host (keyed hashes), token streams on the device (bit-exact)."""
-        ids = np.arange(first_id, first_id + n_records, dtype=np.uint64)
+                  streams=("lp", "old_lp", "ref_lp", "mask"), stream=None, ids=None) -> "PackedBatch":
+        """Synthetic batch: lengths/channels on the host (keyed hashes), token streams on the device (bit-exact).
+        Sample ids are first_id .. first_id + n_records - 1, or `ids` (e.g. a DataLoader batch, loader.py)."""
+        if ids is None:
+            ids = np.arange(first_id, first_id + n_records, dtype=np.uint64)
+        else:
+            ids = np.ascontiguousarray(ids, np.uint64)
+            if len(ids) != n_records:
+                raise ValueError(f"{len(ids)} ids for {n_records} records")
         lens = synth.rollout_lengths(seed, ids, n_roll, dist)
         cu = np.zeros(len(lens) + 1, np.int64)
         np.cumsum(lens, out=cu[1:])
