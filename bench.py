@@ -576,6 +576,9 @@ def cpu_sample():
     return O, sb
 
 
+LOSS_THREADS = os.cpu_count() or 1  # the loss port runs on every host thread (sequences split across them)
+
+
 def cpu_step(O, sb, nthreads):
     """Reference fn_group_advantage + BufferStore reshard (dp8 -> dp4 tp2, B=1 W=8, one thread per worker)
     on records whose payload is the 16 B/token streams (token id, lp, old, ref), then the loss port."""
@@ -587,7 +590,7 @@ def cpu_step(O, sb, nthreads):
     adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
     adv_tok = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
     t2 = time.perf_counter()
-    O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, O.loss_cfg())
+    O.ppo_loss_mt(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, O.loss_cfg(), LOSS_THREADS)
     t3 = time.perf_counter()
     return adv_s + rs_s + (t3 - t2), {"advantage_s": adv_s, "reshard_s": rs_s, "loss_port_s": t3 - t2}
 
@@ -598,10 +601,10 @@ def cpu_baseline(records):
     cpu_step(O, sb, nthreads)  # warm-up
     ts = [cpu_step(O, sb, nthreads)[0] for _ in range(2)]
     t = min(ts)
-    return {"value": round(sb.n_tokens / t, 1), "unit": UNIT, "cores": nthreads, "kind": "reference",
+    return {"value": round(sb.n_tokens / t, 1), "unit": UNIT, "cores": max(nthreads, LOSS_THREADS), "kind": "reference",
             "sample": f"{CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096] ({sb.n_tokens} tokens, 1/16 of C2): "
                       "reference fn_group_advantage + BufferStore dp8->dp4 (B=1,W=8; 8 worker threads) "
-                      "+ oracle loss port (1 thread; the reference has no loss)",
+                      f"+ oracle loss port ({LOSS_THREADS} threads, sequences split; the reference has no loss)",
             "host_cpus": os.cpu_count()}
 
 
@@ -626,9 +629,10 @@ def run_reference(args):
             "dtype": "f64", "data": "synthetic (keyed SplitMix64)", "impl": "reference",
             "config": {"workload": f"bounded sample of C2: {CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096]",
                        "tokens": sb.n_tokens, "phases_s": parts},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": max(nthreads, LOSS_THREADS), "kind": "reference",
                              "sample": f"{sb.n_tokens} tokens; reference fn_group_advantage + BufferStore reshard "
-                                       "(oracle/_ref, compiled from /root/reference) + oracle loss port"},
+                                       "(oracle/_ref, compiled from /root/reference; 8 worker threads) + oracle loss port "
+                                       f"({LOSS_THREADS} threads)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

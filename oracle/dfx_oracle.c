@@ -344,6 +344,68 @@ int dfo_ppo_loss(uint32_t n_seq, const int64_t* cu, const float* lp, const float
   return DFO_OK;
 }
 
+/* Timing-only parallel form of dfo_ppo_loss for the CPU baseline (bench.py): sequences split into nthreads
+ * contiguous slices, each slice run through dfo_ppo_loss, slice means re-weighted by their denominators in slice
+ * order. Same arithmetic per token; the final sums differ from the single-thread order only in rounding.
+ * Unwhitened, no dlogp (both need global denominators first) -- otherwise the single-thread path. */
+typedef struct {
+  uint32_t n_seq;
+  const int64_t* cu;
+  const float *lp, *old_lp, *ref_lp, *adv;
+  const uint8_t* mask;
+  const dfo_loss_cfg* c;
+  dfo_loss_out out;
+  int rc;
+} loss_job;
+
+static void* loss_thread(void* a) {
+  loss_job* j = (loss_job*)a;
+  j->rc = dfo_ppo_loss(j->n_seq, j->cu, j->lp, j->old_lp, j->ref_lp, j->adv, j->mask, j->c, &j->out, NULL);
+  return NULL;
+}
+
+int dfo_ppo_loss_mt(uint32_t n_seq, const int64_t* cu, const float* lp, const float* old_lp,
+                    const float* ref_lp, const float* adv, const uint8_t* mask, const dfo_loss_cfg* c,
+                    dfo_loss_out* out, int nthreads) {
+  if (nthreads <= 1 || c->whiten || n_seq < 2)
+    return dfo_ppo_loss(n_seq, cu, lp, old_lp, ref_lp, adv, mask, c, out, NULL);
+  if ((uint32_t)nthreads > n_seq) nthreads = (int)n_seq;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  loss_job* jobs = (loss_job*)malloc(sizeof(loss_job) * (size_t)nthreads);
+  for (int i = 0; i < nthreads; ++i) {
+    const uint32_t s0 = (uint32_t)((uint64_t)n_seq * (uint64_t)i / (uint64_t)nthreads);
+    const uint32_t s1 = (uint32_t)((uint64_t)n_seq * (uint64_t)(i + 1) / (uint64_t)nthreads);
+    loss_job j = {s1 - s0, cu + s0, lp, old_lp, ref_lp, adv, mask, c, {0}, 0};
+    jobs[i] = j;
+    pthread_create(&th[i], NULL, loss_thread, &jobs[i]);
+  }
+  double N = 0, S = 0, pg = 0, kl = 0, clip = 0, akl = 0;
+  int rc = DFO_OK;
+  for (int i = 0; i < nthreads; ++i) {
+    pthread_join(th[i], NULL);
+    const dfo_loss_out* o = &jobs[i].out;
+    if (jobs[i].rc != DFO_OK) rc = jobs[i].rc;
+    const double d = c->agg == DFO_AGG_TOKEN_MEAN ? o->n_tokens : o->n_seqs;
+    pg += o->pg_loss * d;
+    kl += o->kl * d;
+    clip += o->clipfrac * o->n_tokens;
+    akl += o->approx_kl * o->n_tokens;
+    N += o->n_tokens;
+    S += o->n_seqs;
+  }
+  free(th);
+  free(jobs);
+  const double denom = c->agg == DFO_AGG_TOKEN_MEAN ? N : S;
+  out->pg_loss = denom > 0 ? pg / denom : 0.0;
+  out->kl = denom > 0 ? kl / denom : 0.0;
+  out->loss = out->pg_loss + c->beta * out->kl;
+  out->clipfrac = N > 0 ? clip / N : 0.0;
+  out->approx_kl = N > 0 ? akl / N : 0.0;
+  out->n_tokens = N;
+  out->n_seqs = S;
+  return rc;
+}
+
 /* ---- reshard placement (topology.hpp, data_plane.hpp) ----------------------- */
 
 static int check_layout(uint32_t dp, uint32_t tp, uint32_t world, uint32_t W) {

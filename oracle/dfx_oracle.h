@@ -130,6 +130,10 @@ typedef struct {
 int dfo_ppo_loss(uint32_t n_seq, const int64_t* cu_seqlens, const float* lp, const float* old_lp,
                  const float* ref_lp, const float* adv, const uint8_t* mask,
                  const dfo_loss_cfg* cfg, dfo_loss_out* out, double* dlogp);
+/* timing-only: sequences split over nthreads (CPU baseline); unwhitened, no dlogp, else single-thread. */
+int dfo_ppo_loss_mt(uint32_t n_seq, const int64_t* cu_seqlens, const float* lp, const float* old_lp,
+                    const float* ref_lp, const float* adv, const uint8_t* mask,
+                    const dfo_loss_cfg* cfg, dfo_loss_out* out, int nthreads);
 
 /* ---- topology.hpp + data_plane.hpp: reshard placement ----
  * Producer groups p=0..dp_p-1 hold group_counts[p] records. Returns, for every

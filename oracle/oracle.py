@@ -104,6 +104,7 @@ def _declare_oracle(L):
     L.dfo_gae.argtypes = [u32, P, P, P, P, f64, f64, P, P, P]
     L.dfo_gae.restype = None
     L.dfo_ppo_loss.argtypes = [u32, P, P, P, P, P, P, C.POINTER(LossCfg), C.POINTER(LossOut), P]
+    L.dfo_ppo_loss_mt.argtypes = [u32, P, P, P, P, P, P, C.POINTER(LossCfg), C.POINTER(LossOut), C.c_int]
     L.dfo_reshard_placement.argtypes = [u32, u32, u32, u32, u32, u32, P, P, P]
     L.dfo_serialize_packed.restype = u64
     L.dfo_serialize_packed.argtypes = [u32, P, P, P, P, P, P, C.c_int, P, P, C.c_int, P, P, P]
@@ -269,6 +270,14 @@ def ppo_loss(cu_seqlens, lp, old_lp, ref_lp, adv, mask, cfg: LossCfg, want_grad=
     _check(lib().dfo_ppo_loss(len(cu_seqlens) - 1, ptr(cu_seqlens), ptr(lp), ptr(old_lp), ptr(ref_lp), ptr(adv),
                               ptr(mask), C.byref(cfg), C.byref(out), ptr(g)))
     return out.as_dict(), g
+
+
+def ppo_loss_mt(cu_seqlens, lp, old_lp, ref_lp, adv, mask, cfg: LossCfg, nthreads):
+    """Timing-only parallel form (CPU baseline of bench.py); the checker is ppo_loss."""
+    out = LossOut()
+    _check(lib().dfo_ppo_loss_mt(len(cu_seqlens) - 1, ptr(cu_seqlens), ptr(lp), ptr(old_lp), ptr(ref_lp), ptr(adv),
+                                 ptr(mask), C.byref(cfg), C.byref(out), int(nthreads)))
+    return out.as_dict()
 
 
 # ---- reshard ----------------------------------------------------------------------

@@ -268,3 +268,18 @@ def test_live_reference_random(O):
             continue
         dc2, did, _, _ = O.ref_reshard(B, W, dp_p, tp_p, dp_c, tp_c, gc, np.arange(G, dtype=np.uint64))
         assert (dc == dc2).all() and (idx == did).all()
+
+
+@pytest.mark.parametrize("agg", [0, 1, 2])
+def test_loss_port_threads_match_single_thread(O, agg):
+    """bench.py's CPU baseline times dfo_ppo_loss_mt; it must compute what the single-thread checker computes."""
+    sb = O.SynthBatch(5, 24, 4, O.token_dist("uniform", 0, 1, 700), streams=("lp", "old_lp", "ref_lp", "mask"))
+    adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    at = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
+    cfg = O.loss_cfg()
+    cfg.agg = agg
+    a, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, at, sb.mask, cfg)
+    for nt in (2, 7, 200):
+        b = O.ppo_loss_mt(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, at, sb.mask, cfg, nt)
+        for k in a:
+            assert abs(a[k] - b[k]) <= 1e-12 * max(1.0, abs(a[k])), (nt, k, a[k], b[k])
