@@ -95,3 +95,48 @@ def test_loader_device_batch_bit_exact(O, dfx, shuffle):
         for k in streams:
             assert db.streams[k][:T].cpu().numpy().tobytes() == getattr(sb, k)[:T].tobytes(), (it, k)
         assert db.channels["reward"].cpu().numpy().tobytes() == sb.reward.tobytes()
+
+
+def _loader_worker(rank, world, port, q):
+    """One process per DP group (gloo): each rank loads its own shard; the gathered batches must be the ranks'
+    reference batches in rank order, and together cover the dataset once per epoch without a shuffle."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_13833_b200 as d
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        out = []
+        for shuffle in (False, True):
+            ld = d.make_group_loader(64, world, rank, 13, shuffle)
+            for it in range(4):
+                mine = torch.from_numpy(ld.next_batch_ids(it, 32).astype("int64"))
+                parts = [torch.empty_like(mine) for _ in range(world)]
+                dist.all_gather(parts, mine)
+                out.append((shuffle, it, [p.tolist() for p in parts]))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_loader_gloo_world2(O, dfx):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29300 + (os.getpid() % 400)
+    procs = [ctx.Process(target=_loader_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    for e in range(2):  # iterations 2e, 2e+1: 2 groups x 2 x 16 = one pass over the 64 rows (32-row shards)
+        epoch = sorted(i for shuffle, it, parts in res[0] if it // 2 == e for part in parts for i in part
+                       if not shuffle)
+        assert epoch == list(range(64))
+    if os.path.exists(REF_SO):
+        for shuffle, it, parts in res[0]:
+            for r, part in enumerate(parts):
+                assert part == O.ref_loader_ids(64, 2, r, 13, shuffle, it, 32).tolist()
