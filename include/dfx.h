@@ -117,10 +117,13 @@ dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream s
  * ends by itself): a prep kernel marks rollout ends in a token bitmap, a
  * single-pass decoupled look-back scan over 4096-token CTA tiles does the rest
  * (f32 inputs/outputs, deltas and recurrences in f64), and with whitening a
- * finish kernel reduces the per-tile sums in tile order (deterministic).
+ * finish kernel reduces the per-tile sums in tile order. Outputs are
+ * bit-identical run to run: the look-back composes a data-determined set of
+ * tile records (checkpoint tiles every 32 publish carried inclusives).
  * Workspace (dfx_gae_workspace_bytes) must be zero-filled once at allocation;
  * the kernels keep it consistent across calls (epoch-tagged tile records, the
- * end bitmap cleared as it is consumed), so it can be reused and
+ * end bitmap cleared as it is consumed), so it can be reused -- by calls of
+ * any span up to its capacity: its layout depends only on ws_bytes -- and
  * graph-captured. */
 size_t dfx_gae_workspace_bytes(int64_t n_rollouts, int64_t token_span);
 dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
@@ -130,6 +133,7 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
  * PPO / GRPO clipped surrogate + KL + masked aggregation (new; fills the
  * fn_train slot, distflow/functions.hpp:176-182, node actor_train dag.hpp:335)
  * ------------------------------------------------------------------------- */
+#define DFX_MAX_LOSS_GROUPS 16384
 enum { DFX_KL_NONE = 0, DFX_KL_K1 = 1, DFX_KL_K2 = 2, DFX_KL_K3 = 3 };
 enum { DFX_AGG_TOKEN_MEAN = 0, DFX_AGG_SEQ_MEAN_TOKEN_MEAN = 1, DFX_AGG_SEQ_MEAN_TOKEN_SUM = 2 };
 enum {
@@ -169,7 +173,9 @@ typedef struct dfx_loss_args {
 } dfx_loss_args;
 
 /* Workspace must be zero-filled once at allocation; every call leaves its
- * ticket counters zeroed again. One launch of the fused streaming kernel plus
+ * ticket counters zeroed again. The tickets sit at fixed offsets (any batch
+ * size, at most DFX_MAX_LOSS_GROUPS loss groups), so a workspace can be reused
+ * by calls of any size up to ws_bytes. One launch of the fused streaming kernel plus
  * one finalize launch (two more when dlogp is requested). */
 size_t dfx_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span, int32_t n_loss_groups);
 dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span,
@@ -338,6 +344,11 @@ dfx_status dfx_blob_unpack(const uint8_t* blob, int64_t n_rollouts, const int64_
  * peer-mapped sources copy over NVLink on the caller's stream. */
 dfx_status dfx_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, uint64_t* offset_out);
 dfx_status dfx_ipc_open(const void* handle, size_t handle_bytes, void** base);
+/* Drop one reference taken by dfx_ipc_open on the current device; the mapping
+ * is closed (cudaIpcCloseMemHandle) when the last reference goes. The caller
+ * must have completed every read of it (stream-synchronized). */
+dfx_status dfx_ipc_close(void* base);
+int64_t dfx_ipc_open_count(void); /* live mappings in this process (tests) */
 dfx_status dfx_copy_async(void* dst, const void* src, size_t bytes, dfx_stream stream);
 /* Record metadata of a zero-copy view of records [r0, r1) of a batch, on the device: group_off rebased to the
  * view's first rollout ([r1-r0+1]) and roll_group rebased to r0 ([n_roll] = group_off[r1]-group_off[r0]). */

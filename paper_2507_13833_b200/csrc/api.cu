@@ -62,8 +62,15 @@ dfx_status dfx_event_elapsed_ms(void* b, void* e, float* ms) {
 #include <mutex>
 
 namespace {
+// (device, handle bytes) -> mapped base + reference count. Every dfx_ipc_open takes a reference, dfx_ipc_close
+// drops one and unmaps at zero, so a long run with changing producer allocations does not accumulate mappings
+// (which would pin the producers' freed segments and leak the consumer's address space).
+struct IpcMap {
+  void* base;
+  int64_t refs;
+};
 std::mutex g_ipc_mu;
-std::map<std::pair<int, std::string>, void*> g_ipc_open;  // (device, handle bytes) -> mapped base
+std::map<std::pair<int, std::string>, IpcMap> g_ipc_open;
 }  // namespace
 
 extern "C" {
@@ -77,16 +84,36 @@ dfx_status dfx_ipc_open(const void* handle, size_t handle_bytes, void** base) {
   std::lock_guard<std::mutex> lk(g_ipc_mu);
   auto it = g_ipc_open.find({dev, key});
   if (it != g_ipc_open.end()) {
-    *base = it->second;
+    ++it->second.refs;
+    *base = it->second.base;
     return DFX_OK;
   }
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof(h));
   void* p = nullptr;
   DFX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-  g_ipc_open[{dev, key}] = p;
+  g_ipc_open[{dev, key}] = IpcMap{p, 1};
   *base = p;
   return DFX_OK;
+}
+
+dfx_status dfx_ipc_close(void* base) {
+  int dev = 0;
+  DFX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (auto it = g_ipc_open.begin(); it != g_ipc_open.end(); ++it) {
+    if (it->first.first != dev || it->second.base != base) continue;
+    if (--it->second.refs > 0) return DFX_OK;
+    g_ipc_open.erase(it);
+    DFX_CUDA(cudaIpcCloseMemHandle(base));
+    return DFX_OK;
+  }
+  return dfx::fail(DFX_INVALID_ARGUMENT, "dfx_ipc_close: not a mapping opened by dfx_ipc_open on this device");
+}
+
+int64_t dfx_ipc_open_count(void) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  return (int64_t)g_ipc_open.size();
 }
 
 // base of the cudaMalloc allocation containing ptr: driver cuMemGetAddressRange, resolved at run time so the

@@ -89,37 +89,51 @@ __global__ void __launch_bounds__(256) gae_prep_kernel(const int64_t* __restrict
 }
 
 // ---- the scan ---------------------------------------------------------------------------------------------------
-// Warp-parallel decoupled look-back (warp 0 of the block): the carry X = A at the first token after `tile`.
+// Deterministic look-back (warp 0 of the block): the carry X = A at the first token after `tile`.
+// The carry must not depend on which predecessor records happen to be published when the warp polls (f64
+// composition is not associative), so its definition is fixed by the data alone:
+//   * only tiles whose index is a multiple of 32 ("checkpoints") publish an inclusive record derived from a
+//     carry; every other tile publishes exactly one record, its aggregate -- tagged inclusive when its map is
+//     constant (c == 0: a rollout ends inside the tile, a "natural" inclusive that needs no carry);
+//   * tile t composes the aggregates of tiles t+1 .. W-1 with the inclusive of the next checkpoint W above t, or
+//     stops at the first natural inclusive before W -- the same elements, composed by the same shuffle tree, on
+//     every run.
+// By induction every checkpoint's inclusive, hence every carry and every output bit, is run-to-run identical.
+// Checkpoints chain (W waits for W+32) only across stretches with no rollout end: one L2 round trip per 32 tiles.
+constexpr int64_t kGaeCheckpoint = 32;
+
 __device__ __forceinline__ double gae_lookback(const GaeParams& p, int64_t tile, unsigned int F_AGG,
                                                unsigned int F_INC, int lane) {
   if (tile >= p.n_tiles - 1) return 0.0;
-  Aff G{0.0, 1.0};
-  for (int64_t j0 = tile + 1;; j0 += 32) {
-    const int64_t j = j0 + lane;
-    const bool valid = j < p.n_tiles;
-    ulonglong2 rr = make_ulonglong2(0ull, (unsigned long long)F_INC << 32);  // past the end: A = 0
-    if (valid) rr = rec_load(p.rec + j);
-    for (;;) {
-      const unsigned int tg = rec_tag(rr);
-      const uint32_t inc_m = __ballot_sync(kFull, tg == F_INC);
-      const uint32_t rdy_m = __ballot_sync(kFull, tg == F_AGG || tg == F_INC);
-      const uint32_t need = inc_m ? ((inc_m & (0u - inc_m)) << 1) - 1u : kFull;
+  const int64_t W = (tile / kGaeCheckpoint + 1) * kGaeCheckpoint;
+  const int cnt = (int)(W - tile);  // lanes [0, cnt): tiles tile+1 .. W
+  const int64_t j = tile + 1 + lane;
+  const bool live = lane < cnt && j < p.n_tiles;
+  ulonglong2 rr = make_ulonglong2(0ull, (unsigned long long)F_INC << 32);  // past the end (or unused): A = 0
+  if (live) rr = rec_load(p.rec + j);
+  uint32_t inc_m;
+  for (;;) {
+    const unsigned int tg = rec_tag(rr);
+    inc_m = __ballot_sync(kFull, lane < cnt && tg == F_INC);
+    const uint32_t rdy_m = __ballot_sync(kFull, lane < cnt && (tg == F_AGG || tg == F_INC));
+    if (inc_m) {
+      const uint32_t need = ((inc_m & (0u - inc_m)) << 1) - 1u;
       if ((rdy_m & need) == need) break;
-      if (valid && tg != F_AGG && tg != F_INC) rr = rec_load(p.rec + j);
     }
-    const uint32_t inc_m = __ballot_sync(kFull, rec_tag(rr) == F_INC);
-    const int first = inc_m ? __ffs(inc_m) - 1 : 32;
-    Aff a{0.0, 1.0};
-    if (lane < first) a = Aff{rec_x(rr), rec_c(rr)};
-    else if (lane == first) a = Aff{rec_x(rr), 0.0};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double od = __shfl_down_sync(kFull, a.d, o), oc = __shfl_down_sync(kFull, a.c, o);
-      if (lane + o < 32) a = compose(a, Aff{od, oc});
-    }
-    G = compose(G, Aff{__shfl_sync(kFull, a.d, 0), __shfl_sync(kFull, a.c, 0)});
-    if (first < 32) return G.d;
+    // non-checkpoint tiles publish once (aggregate or natural inclusive); the checkpoint lane waits for F_INC
+    const bool final_rec = tg == F_INC || (tg == F_AGG && lane < cnt - 1);
+    if (live && !final_rec) rr = rec_load(p.rec + j);
   }
+  const int first = __ffs(inc_m) - 1;
+  Aff a{0.0, 1.0};
+  if (lane < first) a = Aff{rec_x(rr), rec_c(rr)};
+  else if (lane == first) a = Aff{rec_x(rr), 0.0};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double od = __shfl_down_sync(kFull, a.d, o), oc = __shfl_down_sync(kFull, a.c, o);
+    if (lane + o < 32) a = compose(a, Aff{od, oc});
+  }
+  return __shfl_sync(kFull, a.d, 0);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     if (lane == 0) rec_store(p.rec + tile, tot.d, (float)tot.c, tot.c == 0.0 ? F_INC : F_AGG);
     const double X = gae_lookback(p, tile, F_AGG, F_INC, lane);
     if (lane == 0) {
-      if (tot.c != 0.0) rec_store(p.rec + tile, fma(tot.c, X, tot.d), 0.0f, F_INC);
+      if (tot.c != 0.0 && tile % kGaeCheckpoint == 0) rec_store(p.rec + tile, fma(tot.c, X, tot.d), 0.0f, F_INC);
       s_X = X;
     }
   }
@@ -376,19 +390,31 @@ int64_t gae_tiles(int64_t token_base, int64_t token_span, int64_t tile) {
 constexpr int64_t kGaeMinTile = 2048;  // smallest tile of any variant (s64: 64 x 32 tokens; workspace sizing)
 
 struct GaeWs {
-  size_t ticket, rec, part, ends, bytes;
+  size_t ticket, ends, rec, part, bytes;
+  int64_t cap_tiles;
 };
-GaeWs gae_ws_layout(int64_t token_span) {
+// The layout is a function of the tile CAPACITY only, never of the call's span: the self-maintained state (the
+// epoch ticket and the all-zero end bitmap) must sit at the same offsets on every call that reuses a workspace, or
+// a call with a smaller span would OR its end bits onto a previous call's tile records / whitening partials.
+// Order: ticket, end bitmap (both kept consistent by the kernels), then the regions written before being read.
+GaeWs gae_ws_layout_cap(int64_t cap_tiles) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  // tile count depends on token_base & 15 as well: size for the worst case (one extra tile)
-  const int64_t nt = (token_span + 15) / kGaeMinTile + 2;
   GaeWs w{};
+  w.cap_tiles = cap_tiles;
   w.ticket = 0;
-  w.rec = al(3 * sizeof(unsigned long long));
-  w.part = w.rec + al(16 * size_t(nt));
-  w.ends = w.part + al(24 * size_t(nt));
-  w.bytes = w.ends + al(size_t(nt) * kGaeMinTile / 8 + 16);
+  w.ends = al(3 * sizeof(unsigned long long));
+  w.rec = w.ends + al(size_t(cap_tiles) * kGaeMinTile / 8 + 16);
+  w.part = w.rec + al(16 * size_t(cap_tiles));
+  w.bytes = w.part + al(24 * size_t(cap_tiles));
   return w;
+}
+// tiles needed for a span (tile count depends on token_base & 15 as well: size for the worst case)
+int64_t gae_tiles_needed(int64_t token_span) { return (token_span + 15) / kGaeMinTile + 2; }
+// the largest capacity whose layout fits in ws_bytes (the caller's buffer size fixes the layout)
+GaeWs gae_ws_layout_fit(size_t ws_bytes) {
+  int64_t cap = (int64_t)(ws_bytes / (kGaeMinTile / 8 + 16 + 24));  // an upper bound; step down to the fit
+  while (cap > 0 && gae_ws_layout_cap(cap).bytes > ws_bytes) --cap;
+  return gae_ws_layout_cap(cap);
 }
 
 // Tuning knob (benchmarking only): DFX_GAE_VARIANT = s128 (default: 128 threads x 32 tokens, 5 CTAs/SM) |
@@ -444,7 +470,7 @@ extern "C" {
 
 size_t dfx_gae_workspace_bytes(int64_t n_rollouts, int64_t token_span) {
   (void)n_rollouts;
-  return gae_ws_layout(token_span).bytes;
+  return gae_ws_layout_cap(gae_tiles_needed(token_span)).bytes;
 }
 
 dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam, float* adv,
@@ -455,8 +481,9 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
     if (whiten) DFX_CUDA(cudaMemsetAsync(whiten, 0, 3 * sizeof(double), stream));
     return DFX_OK;
   }
-  const GaeWs wl = gae_ws_layout(token_span);
-  if (!workspace || ws_bytes < wl.bytes) return fail(DFX_INVALID_ARGUMENT, "dfx_gae: workspace too small");
+  const GaeWs wl = gae_ws_layout_fit(ws_bytes);
+  if (!workspace || wl.cap_tiles < gae_tiles_needed(token_span))
+    return fail(DFX_INVALID_ARGUMENT, "dfx_gae: workspace too small");
   char* w = static_cast<char*>(workspace);
   GaeParams p{};
   p.cu = b->cu_seqlens;

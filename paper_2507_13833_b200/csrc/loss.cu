@@ -661,16 +661,22 @@ LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t n_slots, int32_t n_grou
     off += align_up(bytes);
     return p;
   };
-  // ticket first: callers zero the workspace once at allocation, and the
-  // kernels restore it to zero on exit
-  w.ticket = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * 2 * size_t(n_groups)));
+  // the self-maintained tickets first, at offsets that do not depend on the call (callers zero the workspace once
+  // at allocation and the kernels restore the tickets to zero on exit; a call with different sizes must find them
+  // where the previous call left them); then the regions every call writes before reading
   w.slot_ticket = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (kMaxLossSrc + 1)));
+  w.ticket = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * 2 * size_t(DFX_MAX_LOSS_GROUPS)));
   w.part = reinterpret_cast<double*>(take(sizeof(double) * 5 * size_t(n_slots)));
   w.blk = reinterpret_cast<double*>(take(sizeof(double) * 6 * size_t(n_groups) * size_t(w.nb)));
   w.seq_n = reinterpret_cast<double*>(take(sizeof(double) * size_t(n_seq + 1)));
   w.grp_stats = reinterpret_cast<double*>(take(sizeof(double) * 2 * size_t(n_groups)));
   w.bytes = off;
   return w;
+}
+
+// slots of one source; a source without rollouts owns none (its cu_seqlens may be NULL and is never read)
+int64_t src_slots(int64_t n_rollouts, int64_t token_span) {
+  return n_rollouts > 0 ? slot_count(n_rollouts, token_span, slot_shift(token_span)) : 0;
 }
 
 SlotGeom geom_of(const dfx_packed* b, int64_t base, int64_t span) {
@@ -796,7 +802,7 @@ size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_sr
   int64_t S = 0, U = 0;
   for (int32_t k = 0; srcs && k < n_src; ++k) {
     S += srcs[k].b.n_rollouts;
-    U += slot_count(srcs[k].b.n_rollouts, srcs[k].token_span, slot_shift(srcs[k].token_span));
+    U += src_slots(srcs[k].b.n_rollouts, srcs[k].token_span);
   }
   return loss_ws_layout(nullptr, S, U, n_loss_groups).bytes;
 }
@@ -810,6 +816,7 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
   if (!srcs || n_src < 1 || !cfg || !args || !args->out) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
   if (n_src > kMaxLossSrc) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: at most 4 sources");
   const int32_t ng = args->n_loss_groups < 1 ? 1 : args->n_loss_groups;
+  if (ng > DFX_MAX_LOSS_GROUPS) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: more than DFX_MAX_LOSS_GROUPS loss groups");
   int64_t S = 0, U = 0;
   for (int32_t k = 0; k < n_src; ++k) S += srcs[k].b.n_rollouts;
   if (S <= 0) {
@@ -855,7 +862,7 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
     src[k].adv_tok_in = x.adv_tok_in;
     src[k].adv_tok_out = x.adv_tok_out;
     src[k].dlogp = x.dlogp;
-    U += slot_count(b->n_rollouts, x.token_span, slot_shift(x.token_span));
+    U += src_slots(b->n_rollouts, x.token_span);
   }
   const LossWs w = loss_ws_layout(workspace, S, U, ng);
   if (!workspace || ws_bytes < w.bytes) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: workspace too small");

@@ -74,6 +74,10 @@ def _declare():
     L.dfx_ipc_export.restype = C.c_int32
     L.dfx_ipc_open.argtypes = [P, C.c_size_t, C.POINTER(C.c_void_p)]
     L.dfx_ipc_open.restype = C.c_int32
+    L.dfx_ipc_close.argtypes = [P]
+    L.dfx_ipc_close.restype = C.c_int32
+    L.dfx_ipc_open_count.argtypes = []
+    L.dfx_ipc_open_count.restype = C.c_int64
     L.dfx_copy_async.argtypes = [P, P, C.c_size_t, P]
     L.dfx_copy_batch.argtypes = [C.c_int64, P, P, P, P]
     L.dfx_copy_batch.restype = C.c_int32
@@ -203,6 +207,19 @@ class ConsumerBatch:
     bytes_recv: int = 0
     sources: list | None = None   # lazy: per group, [PackedBatch | RemoteSource]
     release: object = None        # lazy: callable issuing the closing device barrier
+    ipc_bases: list | None = None  # peer mappings this exchange opened (dfx_ipc_open); see close_mappings()
+    template_owned: bool = False   # a store / exchange template holds this batch's mappings beyond its iteration
+
+    def close_mappings(self) -> None:
+        """Drop the references this exchange took on peer mappings (the store calls it when the batch -- or the
+        template holding it -- is retired). Every read of them must have completed: the stream is synchronized."""
+        if not self.ipc_bases:
+            return
+        torch.cuda.current_stream().synchronize()
+        L = _declare()
+        for b in self.ipc_bases:
+            _abi.check(L.dfx_ipc_close(C.c_void_p(b)))
+        self.ipc_bases = None
 
     def group_view(self, d: int) -> PackedBatch:
         i = self.groups.index(d)
@@ -292,9 +309,9 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     sizes = np.zeros((nseg, 6), np.int64)
     for i, (b, r0, r1, s0, s1, t0, t1) in loc.items():
         sizes[i] = (s1 - s0, t1 - t0, t0 & 15, t0, s0, r0)
-    peer_addr = {}
+    peer_addr, opened = {}, []
     if pull:
-        sizes, peer_addr = _gather_pull_tables(plan, loc, sizes, group, meta_group, ch_names, stream_specs)
+        sizes, peer_addr, opened = _gather_pull_tables(plan, loc, sizes, group, meta_group, ch_names, stream_specs)
     elif distributed:
         sizes = all_reduce_host(sizes, group, meta_group, dev)
     t_ = _mark("sizes", t_)
@@ -324,9 +341,12 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
             view = b0 if (r_a == 0 and r_b == b0.n_records) else b0.view_records(r_a, r_b)
             if pull:  # peers may pull from us: take part in both barriers
                 _device_barrier(group, dev)
-                _device_barrier(group, dev)
                 sent = sum(int(sizes[i, 1]) for i, (d, p, *_r) in enumerate(plan.segs) if i in loc
                            for r in plan.dst_ranks[d] if r != rank)
+                if lazy:  # the closing barrier is issued at release(), in step with the lazy consumers'
+                    return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0,
+                                         release=lambda: _device_barrier(group, dev))
+                _device_barrier(group, dev)
                 return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0)
             _, sent, recv_b, _ = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)
             return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, recv_b)
@@ -354,7 +374,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
         recv_b = sum(int(sizes[i, 1]) * sum(torch.empty(0, dtype=dt_).element_size() for dt_ in stream_specs.values())
                      for i in order if i not in loc)
         return ConsumerBatch(None, groups, rec_off, roll_off, False, 0, recv_b, per_group,
-                             release=lambda: _device_barrier(group, dev))
+                             release=lambda: _device_barrier(group, dev), ipc_bases=opened)
 
     # 3. allocate the consumer batch
     R, S, T = rec_off[-1], roll_off[-1], tok_off[-1]
@@ -432,7 +452,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     t_ = _mark("unpack", t_)
     # host offsets of the consumer batch are fetched lazily (PackedBatch.ensure_host_meta): no D2H here
     out.host_group_off, out.host_cu = None, None
-    cbatch = ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b)
+    cbatch = ConsumerBatch(out, groups, rec_off, roll_off, False, sent, recv_b, ipc_bases=opened)
     if pull and templates is not None and template_key is not None:
         # record this exchange as a template: every copy as (stream, offset in the consumer stream, source
         # address, bytes), the unpack segments, and (after one D2H, only now) the consumer's host offsets
@@ -453,9 +473,12 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
         templates[template_key] = {"R": R, "S": S, "T": T, "ch": list(ch_names), "specs": dict(stream_specs),
                                    "copies": copies, "metas": (SegMeta * len(metas))(*metas), "n_metas": len(metas),
                                    "groups": groups, "rec_off": rec_off, "roll_off": roll_off, "sent": sent,
-                                   "recv": recv_b, "h_go": out.host_group_off, "h_cu": out.host_cu}
+                                   "recv": recv_b, "h_go": out.host_group_off, "h_cu": out.host_cu,
+                                   "ipc": cbatch}
+        cbatch.template_owned = True  # the template's replays read these mappings: it owns them now
         if len(templates) > 8:
-            templates.pop(next(iter(templates)))
+            old_t = templates.pop(next(iter(templates)))
+            old_t["ipc"].close_mappings()
     return cbatch
 
 
@@ -487,6 +510,23 @@ def reuse_lazy(prev: ConsumerBatch, group) -> ConsumerBatch:
     _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
     return ConsumerBatch(None, prev.groups, prev.rec_off, prev.roll_off, False, prev.bytes_sent, prev.bytes_recv,
                          prev.sources, release=lambda: _device_barrier(group, dev))
+
+
+def reuse_zero_copy(prev: ConsumerBatch, plan: Plan, sources: dict, group) -> ConsumerBatch:
+    """A lazy step on a rank whose consumer groups were a zero-copy view last time, with every rank's producer
+    batches unchanged (the store's template hit, taken by all ranks alike): the same view over this step's
+    producer batch (host-only), and the same two barriers as the lazy consumers -- the first now, the second at
+    release()."""
+    loc = _src_slices(plan, sources)
+    order = [i for d in prev.groups for i, sg in enumerate(plan.segs) if sg[0] == d]
+    b0, r_a, r_b = loc[order[0]][0], loc[order[0]][1], loc[order[-1]][2]
+    view = b0 if (r_a == 0 and r_b == b0.n_records) else b0.view_records(r_a, r_b)
+    if not _distributed(group):
+        return ConsumerBatch(view, prev.groups, prev.rec_off, prev.roll_off, True, 0, 0)
+    dev = view.device
+    _device_barrier(group, dev)
+    return ConsumerBatch(view, prev.groups, prev.rec_off, prev.roll_off, True, prev.bytes_sent, 0,
+                         release=lambda: _device_barrier(group, dev))
 
 
 _BARRIER = {}
@@ -565,7 +605,7 @@ def _gather_pull_tables(plan: Plan, loc: dict, sizes, group, meta_group, ch_name
     table = np.zeros_like(sizes)
     for i, (d, p, *_x) in enumerate(plan.segs):
         table[i] = allrows[plan.src_rank[p], i * 6:(i + 1) * 6]
-    addr = {}
+    addr, opened = {}, []
     for i, (d, p, *_x) in enumerate(plan.segs):
         src = plan.src_rank[p]
         if src == plan.rank or plan.rank not in plan.dst_ranks[d] or (src, int(p)) in addr:
@@ -575,9 +615,10 @@ def _gather_pull_tables(plan: Plan, loc: dict, sizes, group, meta_group, ch_name
         for j, n in enumerate(names):
             base = C.c_void_p()
             _abi.check(L.dfx_ipc_open(rows[j, :8].tobytes(), 64, C.byref(base)))
+            opened.append(base.value)
             out[n] = base.value + int(rows[j, 8])
         addr[(src, int(p))] = out
-    return table, addr
+    return table, addr, opened
 
 
 def all_reduce_host(a: np.ndarray, group, meta_group, dev) -> np.ndarray:

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 from . import errors
 from .packed import PackedBatch
-from .reshard import ConsumerBatch, Layout, Plan, Topology, exchange, reuse_lazy
+from .reshard import ConsumerBatch, Layout, Plan, Topology, exchange, reuse_lazy, reuse_zero_copy
 
 
 def _signature(batches) -> int:
@@ -65,6 +65,7 @@ class DeviceBufferStore:
         self._templates: dict = {}   # stage -> (key, lazy ConsumerBatch) for reuse when nothing changed
         self._mat_templates: dict = {}  # (plan key, signatures) -> materialized pull template (reshard.exchange)
         self.template_hits = 0
+        self._retired: list = []     # replaced lazy templates whose peer mappings close at the next worker_done
         self.low_water = 0
         self.suppressed = 0
         self.bytes_sent = 0
@@ -121,15 +122,22 @@ class DeviceBufferStore:
         tmpl = self._templates.get(stage)
         if lazy and tmpl is not None and tmpl[0] == tkey:
             # same producer batches everywhere as last time (same memory, same extents): reuse the mapped
-            # consumer sources, no table exchange -- only the ordering barrier
-            e.ready = reuse_lazy(tmpl[1], self.group)
+            # consumer sources, no table exchange -- only the ordering barriers. tkey holds every rank's
+            # signature and every rank records a template after every lazy exchange (zero-copy ones too), so
+            # all ranks take this branch together and issue the same collectives
+            prev = tmpl[1]
+            e.ready = (reuse_zero_copy(prev, plan, sources, self.group) if prev.sources is None
+                       else reuse_lazy(prev, self.group))
             self.template_hits += 1
         else:
             e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
                                transport=self.transport, lazy=lazy, templates=self._mat_templates,
                                template_key=tkey)
-            if lazy and e.ready.sources is not None:
+            if lazy:
+                if tmpl is not None:
+                    self._retired.append(tmpl[1])  # its mappings close once this iteration retires
                 self._templates[stage] = (tkey, e.ready)
+                e.ready.template_owned = True
         e.consumed = to
         e.by_group = {}
         self.bytes_sent += e.ready.bytes_sent
@@ -176,6 +184,12 @@ class DeviceBufferStore:
                 e.ready.release()
                 e.ready.release = None
         self.low_water = max(self.low_water, iteration + 1)
+        for k, e in self._entries.items():  # retire the peer mappings of purged, template-less exchanges
+            if k[1] < self.low_water and e.ready is not None and not getattr(e.ready, "template_owned", False):
+                e.ready.close_mappings()
+        for t in self._retired:
+            t.close_mappings()
+        self._retired = []
         self._entries = {k: v for k, v in self._entries.items() if k[1] >= self.low_water}
 
     def suppressed_count(self) -> int:

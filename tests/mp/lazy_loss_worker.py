@@ -18,6 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 import paper_2507_13833_b200 as dfx  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from tests.helpers import assert_rel  # noqa: E402
 from paper_2507_13833_b200.reshard import Layout, RemoteSource, Topology  # noqa: E402
 from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan  # noqa: E402
 
@@ -60,6 +62,15 @@ for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("unif
     np.testing.assert_allclose(got[:5], want[:5], rtol=2e-6, atol=1e-9)
     assert split[5] == want[5] and split[6] == want[6], (split, want)
     np.testing.assert_allclose(split[:5], want[:5], rtol=2e-6, atol=1e-9)
+    # and all three against the CPU ORACLE on the consumer group's records (both producer groups, in order)
+    sb = O.SynthBatch(5 + it, world * R, 4, O.token_dist(dist_kind, 0, 1, hi))
+    adv_o = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    ref_o, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp,
+                          O.broadcast_advantage(sb.cu_seqlens, adv_o, sb.mask), sb.mask, O.loss_cfg())
+    for name, row in (("lazy multi-source", got), ("tp-split fold", split), ("materialized", want)):
+        assert row[5] == ref_o["n_tokens"] and row[6] == ref_o["n_seqs"], (name, row, ref_o)
+        for k, j in (("loss", 0), ("pg_loss", 1), ("kl", 2), ("clipfrac", 3), ("approx_kl", 4)):
+            assert_rel(row[j], ref_o[k], f"{k} {name} case {it} rank {rank}")
     # per-token advantages: source k's tokens land at the consumer's cumulative token offset
     want_tok = ref["adv_tok"].cpu().numpy()
     off = 0

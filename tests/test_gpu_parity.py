@@ -190,7 +190,7 @@ def test_loss_groups_match_slices(O, dfx):
         cu = np.ascontiguousarray(sb.cu_seqlens[lgo[g]:lgo[g + 1] + 1])
         ref, _ = O.ppo_loss(cu, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, cfg)
         assert out[g][5] == ref["n_tokens"]
-        assert_close_scalar(out[g][0], ref["loss"], 1.0, f"group {g} loss")
+        assert_close_scalar(out[g][0], ref["loss"], 1.0, f"loss group {g}")
 
 
 def test_empty_and_degenerate(O, dfx):
@@ -323,9 +323,10 @@ def test_batch_on_non_current_device(dfx):
         outs.append((b.channels["advantage"].cpu().numpy(), b.streams["advantage"][:b.token_span].cpu().numpy(),
                      res["out"].cpu().numpy()))
     assert outs[0][0].tobytes() == outs[1][0].tobytes()  # group advantage: bit-exact
-    # GAE's look-back may combine a different set of predecessor tiles run to run (f64 rounding), hence a tolerance
-    np.testing.assert_allclose(outs[1][1], outs[0][1], rtol=1e-6, atol=1e-6)
-    np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-6, atol=1e-9)
+    # GAE's look-back composes a data-determined set of tile records: bit-exact across runs and devices, and so
+    # is the loss that consumes it (fixed-order reductions)
+    assert outs[0][1].tobytes() == outs[1][1].tobytes()
+    assert outs[0][2].tobytes() == outs[1][2].tobytes()
 
 
 @pytest.mark.parametrize("agg", ["token-mean", "seq-mean-token-sum", "seq-mean-token-mean"])

@@ -244,6 +244,24 @@ def test_two_gpu_lazy_reshard_fused_loss():
     assert r.stdout.count("LAZY_OK") == 2, r.stdout[-2000:]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_gpus", [2, 4])
+def test_mixed_zero_copy_lazy_reshard(n_gpus):
+    """Zero-copy and peer-reading GPUs in one lazy reshard, several iterations over the same producer batches and a
+    collective in between: no deadlock, every group's loss equals the oracle, peer mappings do not accumulate
+    (tests/mp/mixed_lazy_worker.py)."""
+    if torch.cuda.device_count() < n_gpus:
+        pytest.skip(f"needs {n_gpus} GPUs")
+    port = 28600 + n_gpus * 50 + (os.getpid() % 40)
+    r = subprocess.run(["timeout", "300", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n_gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "mp", "mixed_lazy_worker.py")],
+                       capture_output=True, text=True, timeout=360, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("MIXED_OK") == n_gpus, r.stdout[-2000:]
+    print(r.stdout[-1500:])
+
+
 def _metrics_worker(rank, world, port, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
