@@ -365,6 +365,92 @@ dfx_status dfx_copy_batch(int64_t n, const uint64_t* dst, const uint64_t* src, c
                           dfx_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * Distributed DataBuffer: the reference's BufferStore (distflow/data_plane.hpp:
+ * 225-457) for one process per GPU, native end to end. Replaces put /
+ * ensure_ready / exchange / get and the all_to_all behind them
+ * (data_plane.hpp:400-442, transport.hpp:718-754): one host call per verb, no
+ * Python and no host-side collective library on the data path.
+ *
+ * Communicator: an NCCL communicator over the participating GPUs (one rank per
+ * process). Rank 0 makes the id (dfx_comm_unique_id) and ships its bytes to the
+ * others by any side channel (a pipe, a file, torch's TCPStore); every rank
+ * then calls dfx_comm_init with its device current.
+ * ------------------------------------------------------------------------- */
+#define DFX_COMM_ID_BYTES 128
+#define DFX_MAX_CH 4
+#define DFX_MAX_STREAMS 8
+typedef struct dfx_comm dfx_comm;
+dfx_status dfx_comm_unique_id(void* id_out /* DFX_COMM_ID_BYTES */);
+dfx_status dfx_comm_init(const void* id, int32_t n_ranks, int32_t rank, dfx_comm** out);
+dfx_status dfx_comm_destroy(dfx_comm* comm);
+int32_t dfx_comm_rank(const dfx_comm* comm);
+int32_t dfx_comm_size(const dfx_comm* comm);
+/* Sum of n int64 values over the ranks, host in / host out (one device
+ * all-reduce on the stream + a D2H read; synchronizes the stream). */
+dfx_status dfx_comm_allreduce_i64(dfx_comm* comm, const int64_t* in, int64_t* out, int64_t n, dfx_stream stream);
+
+/* A device batch in a store's schema (generic form of dfx_packed): streams and
+ * channels in the schema's order; group_off is relative (group_off[0] == 0);
+ * cu_seqlens are absolute token indices into the streams (st[k] points at token
+ * 0 of the coordinate system). h_group_off / h_cu: host copies (the store plans
+ * from them; it never reads device metadata on the host). */
+typedef struct dfx_batch {
+  int64_t n_records, n_rollouts, token_base, token_span;
+  const uint64_t* ids;
+  const int32_t* group_off;
+  const int32_t* roll_group;
+  const int64_t* cu_seqlens;
+  const double* ch[DFX_MAX_CH];
+  const void* st[DFX_MAX_STREAMS];
+  const int32_t* h_group_off;
+  const int64_t* h_cu;
+} dfx_batch;
+
+typedef struct dfx_dstore_cfg {
+  uint32_t num_nodes, workers_per_node;  /* the reference's B x W logical world (topology.hpp:11-35) */
+  const int32_t* rank_of_worker;         /* [B*W]: the process (GPU) rank hosting each logical worker */
+  int32_t n_streams;                     /* token streams per rollout (<= DFX_MAX_STREAMS) */
+  const uint32_t* stream_esz;            /* their element sizes in bytes */
+  int32_t n_ch;                          /* f64 rollout channels (<= DFX_MAX_CH) */
+  int32_t n_stages;
+  const char* const* stage_names;        /* StoreStagePlan per stage (data_plane.hpp:216-220) */
+  const uint32_t* produced_dp;
+  const uint32_t* produced_tp;
+  const uint32_t* consumed_dp;           /* 0: the layout is given to ensure_ready (fallback_to_layout) */
+  const uint32_t* consumed_tp;
+} dfx_dstore_cfg;
+typedef struct dfx_dstore dfx_dstore;
+
+/* All work is enqueued on `stream` (the caller's compute stream, so consumers
+ * are ordered after the exchange with no extra synchronization). */
+dfx_status dfx_dstore_create(const dfx_dstore_cfg* cfg, dfx_comm* comm, dfx_stream stream, dfx_dstore** out);
+dfx_status dfx_dstore_destroy(dfx_dstore* s);
+/* BufferStore::put (data_plane.hpp:237-264): TP != 0 is suppressed (*accepted
+ * = 0); the group must be local to this rank; duplicates and stale iterations
+ * are errors. The batch's memory must stay valid until ensure_ready returns
+ * (the exchange reads it on the stream). */
+dfx_status dfx_dstore_put(dfx_dstore* s, const char* stage, uint64_t iteration, uint32_t dp, uint32_t tp,
+                          const dfx_batch* batch, int32_t* accepted);
+/* BufferStore::ensure_ready / exchange (:296-346, :400-442), collective over
+ * the communicator: one all-reduce of the producer sizes (cached plan when they
+ * repeat), then the reshard on the stream -- metadata pack kernel, ONE grouped
+ * NCCL send/recv of every cross-GPU segment (token streams straight from the
+ * producer's streams into the consumer's, 16-byte aligned or staged), local
+ * segments by one copy kernel on a forked stream, one unpack kernel. Consumer
+ * groups that are one contiguous local run are zero-copy views. DFX_NOT_READY
+ * if a local producer group has not put. */
+dfx_status dfx_dstore_ensure_ready(dfx_dstore* s, const char* stage, uint64_t iteration, uint32_t to_dp,
+                                   uint32_t to_tp);
+/* BufferStore::get (:269-292): consumer group dest_dp's batch on this GPU (TP
+ * peers on one GPU share it), valid until worker_done retires the iteration. */
+dfx_status dfx_dstore_get(dfx_dstore* s, const char* stage, uint64_t iteration, uint32_t dest_dp, uint32_t to_dp,
+                          uint32_t to_tp, dfx_batch* out);
+/* BufferStore::worker_done (:351-367): once per local logical worker. */
+dfx_status dfx_dstore_worker_done(dfx_dstore* s, uint64_t iteration);
+/* {suppressed puts, NVLink bytes sent, NVLink bytes received, local bytes copied, plan cache hits} */
+dfx_status dfx_dstore_stats(const dfx_dstore* s, uint64_t* out5);
+
+/* ---------------------------------------------------------------------------
  * Timing helpers (cudaEvent_t as void*), so ctypes callers can bracket a
  * kernel on the stream it runs on.
  * ------------------------------------------------------------------------- */

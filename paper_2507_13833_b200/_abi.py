@@ -11,7 +11,8 @@ import os
 from . import errors
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libdfx.so")
+# DFX_LIB_PATH: an alternative in-tree build of the same library (kernel variant sweeps, tools/build_variant.py)
+LIB_PATH = os.environ.get("DFX_LIB_PATH") or os.path.join(PKG, "lib", "libdfx.so")
 
 P = C.c_void_p
 i32, i64, u64, f64, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t

@@ -182,16 +182,26 @@ __device__ __forceinline__ bool slot_unit(const SlotGeom& g, int64_t u, int lane
   return true;
 }
 
-// Host: window size of the streaming kernels. 2048-token windows: measured on
-// B200, shorter windows lose more to per-slot setup (search + reduction) than
-// they gain in balance, even for 4M-token batches.
+// Host: window size of the streaming kernels, a function of the token span only (the workspace sizing and the
+// launch must agree): 2048-token windows. Measured on B200: shorter windows lose more to per-slot setup (search +
+// reduction + partials) than they gain in balance -- at C2's 33.5M tokens and also at C3's 4.2M (2048 windows for
+// ~3.5k resident warps; 512-token windows made the C3 step 20% slower, profiles/r02_clip_sweep2.log).
+// Benchmarking knobs: DFX_SLOT_SHIFT forces the window; DFX_SLOT_TARGET=k halves it until there are k windows per
+// resident warp.
 inline int slot_shift(int64_t token_span) {
-  (void)token_span;
-  static const int sh = [] {
-    const char* e = std::getenv("DFX_SLOT_SHIFT");  // tuning knob (benchmarking only)
-    const int v = e ? std::atoi(e) : 11;
-    return v >= 8 && v <= 14 ? v : 11;
+  static const int forced = [] {
+    const char* e = std::getenv("DFX_SLOT_SHIFT");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 8 && v <= 14 ? v : 0;
   }();
+  if (forced) return forced;
+  static const int64_t target = [] {
+    const char* e = std::getenv("DFX_SLOT_TARGET");
+    const int v = e ? std::atoi(e) : 0;
+    return int64_t(v >= 1 && v <= 64 ? v : 0) * 148 * 24;
+  }();
+  int sh = 11;
+  while (target && sh > 8 && (token_span >> sh) < target) --sh;
   return sh;
 }
 

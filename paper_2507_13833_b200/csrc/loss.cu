@@ -6,10 +6,18 @@
 // :163-172 (fn_ppo_advantage), :176-182 (fn_train slot the loss fills).
 // HBM-bound streaming kernels: no tensor cores (no dense contraction).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
 #include "common.cuh"
+
+#ifndef DFX_CLIP_MODE
+#define DFX_CLIP_MODE 0
+#endif
+#ifndef DFX_TOKEN_MINB
+#define DFX_TOKEN_MINB 2
+#endif
 
 namespace dfx {
 
@@ -119,6 +127,10 @@ struct LossParams {
   const double* whiten_sums;
   int whiten;
   float clip_lo, clip_hi, beta;
+  // clip decision thresholds on the log-ratio d = lp - old: rho > 1+eps_hi  <=>  d > log(1+eps_hi), rho < 1-eps_lo
+  // <=> d < log(1-eps_lo), each as a float pair T32 + Tlo (clip_twosum)
+  float t_hi32, t_lo32;
+  float t_hi32_lo, t_lo32_lo;  // T64 - T32 (the thresholds as float pairs)
   double adv_eps;
   int kl_type;
   int agg;
@@ -157,21 +169,37 @@ struct TokAcc {
 // never clipped -- identical to the reference formula.
 struct UnitAdv {
   float A, nA, s, sb;
+  float sT32;   // s * log-ratio threshold (A > 0: log(1+eps_hi), A < 0: log(1-eps_lo)); +inf when A == 0
 };
-__device__ __forceinline__ UnitAdv unit_adv(float A, float lo, float hi) {
+__device__ __forceinline__ UnitAdv unit_adv(float A, float lo, float hi, float t_lo32, float t_hi32) {
   UnitAdv u;
   u.A = A;
   u.nA = -fabsf(A);
   u.s = A < 0.0f ? -1.0f : 1.0f;
-  u.sb = A > 0.0f ? hi : (A < 0.0f ? -lo : __int_as_float(0x7f800000));
+  const float inf = __int_as_float(0x7f800000);
+  u.sb = A > 0.0f ? hi : (A < 0.0f ? -lo : inf);
+  u.sT32 = A > 0.0f ? t_hi32 : (A < 0.0f ? -t_lo32 : inf);
   return u;
+}
+
+// The clip fires iff s*(lp - old) > s*T, T the log-ratio threshold of A's sign (log(1+eps_hi) for A > 0,
+// log(1-eps_lo) for A < 0): the same decision as the reference formula's pg2 > pg1 on exp(lp - old) in f64
+// (oracle/dfx_oracle.c), made exactly in f32 arithmetic, branch-free: TwoSum gives d + e == lp - old exactly
+// (d = f32(lp - old)), the threshold is the float pair T32 + Tlo == T64 to ~2^-48, and s*d - s*T32 is exact
+// wherever the sign of the total is in doubt (Sterbenz), so the sum's sign is the exact comparison. Keeps clipfrac
+// (a count) exact instead of within f32 rounding of exp and 1+eps. A == 0: s*T32 = +inf, never clipped.
+__device__ __forceinline__ bool clip_twosum(const LossParams& p, float s, float sT32, float l, float o, float d) {
+  const float bb = d - l;
+  const float e = (l - (d - bb)) + (-o - bb);
+  const float sTl = s > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo;
+  return (s * d - sT32) + (s * e - sTl) > 0.0f;
 }
 
 // Four tokens of one aligned vector starting at token t. FULL: all in range.
 template <int ADV, int KL, bool DLOGP, bool FULL>
 __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua, float4 lv, float4 ov, float4 rv,
-                                         float4 av, uint32_t mk, int64_t t, int64_t t0, int64_t t1, float mu,
-                                         float rstd, float w, TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
+                                         float4 av, uint32_t mk, int64_t t, int64_t t0, int64_t t1, double mu,
+                                         double rstd, float w, TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
   const float lo = 1.0f - p.clip_lo, hi = 1.0f + p.clip_hi;
   float x[4], kl[4], dkl[4];
 #pragma unroll
@@ -198,27 +226,44 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
 #pragma unroll
     for (int k = 0; k < 4; ++k) { kl[k] = 0.0f; dkl[k] = 0.0f; }
   }
+  // per-token log ratio and the exact clip decision (clip_twosum): for a warp-uniform advantage (GRPO broadcast /
+  // per-rollout) here, for per-token advantages (GAE) in the loop below
+  float dd[4];
+  bool cl[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) dd[k] = f4_get(lv, k) - f4_get(ov, k);  // log ratio
+  // DFX_CLIP_MODE (kernel-variant sweeps only): 0 the exact decision below (default); 2 the f32 log-ratio
+  // decision alone (can differ from the reference for tokens within an f32 ulp of the threshold); 3 the ratio
+  // decision s*rho > s*bound of round 1 (within a few f32 ulps). Measured at C2: 2 is ~2.5% faster than 0.
+  if constexpr (ADV != DFX_ADV_TOKEN && DFX_CLIP_MODE != 3) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      cl[k] = DFX_CLIP_MODE == 2 ? ua.s * dd[k] > ua.sT32
+                                 : clip_twosum(p, ua.s, ua.sT32, f4_get(lv, k), f4_get(ov, k), dd[k]);
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     bool on = ((mk >> (8 * k)) & 0xffu) != 0u;
     if (!FULL) on = on && (t + k >= t0) && (t + k < t1);
     const float m = on ? 1.0f : 0.0f;
-    const float l = f4_get(lv, k), o = f4_get(ov, k);
-    const float d = l - o;                    // log ratio
+    const float d = dd[k];
     const float rho = exp2f(d * kLog2e);     // MUFU.EX2, ~2 ulp
-    float pg, clipf, A;
-    if (ADV == DFX_ADV_TOKEN) {
-      A = (f4_get(av, k) - mu) * rstd;        // mu = 0, rstd = 1 unless whitening
+    float A, pg;
+    if constexpr (ADV == DFX_ADV_TOKEN) {
+      // whitening in f64 (mu, rstd f64): the f32 rounding of mu would shift every advantage alike
+      A = p.whiten ? (float)(((double)f4_get(av, k) - mu) * rstd) : f4_get(av, k);
       const float rc = fminf(fmaxf(rho, lo), hi);
-      const float pg1 = -A * rho, pg2 = -A * rc;
-      pg = fmaxf(pg1, pg2);
-      clipf = pg2 > pg1 ? 1.0f : 0.0f;
+      pg = fmaxf(-A * rho, -A * rc);
+      const float s = A < 0.0f ? -1.0f : 1.0f;
+      const float sT = A > 0.0f ? p.t_hi32 : (A < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
+      cl[k] = clip_twosum(p, s, sT, f4_get(lv, k), f4_get(ov, k), d);
     } else {
       A = ua.A;
       const float sr = ua.s * rho;
       pg = ua.nA * fminf(sr, ua.sb);
-      clipf = sr > ua.sb ? 1.0f : 0.0f;
+      if constexpr (DFX_CLIP_MODE == 3) cl[k] = sr > ua.sb;
     }
+    const float clipf = cl[k] ? 1.0f : 0.0f;
     acc.pg = fmaf(m, pg, acc.pg);
     acc.kl = fmaf(m, kl[k], acc.kl);
     acc.akl = fmaf(-m, d, acc.akl);
@@ -281,6 +326,15 @@ __device__ __forceinline__ void store_vec(float* base, int64_t t, int64_t t0, in
   }
 }
 
+// masked whitening of the advantages, unbiased variance + 1e-8 (oracle/dfx_oracle.c dfo_ppo_loss)
+__device__ __forceinline__ void whiten_coeffs(const LossParams& p, double& mu, double& rstd) {
+  const double N = p.whiten_sums[2];
+  const double m1 = N > 0 ? p.whiten_sums[0] / N : 0.0;
+  const double var = N > 1 ? (p.whiten_sums[1] - p.whiten_sums[0] * m1) / (N - 1.0) : 0.0;
+  mu = m1;
+  rstd = 1.0 / sqrt(fmax(var, 0.0) + 1e-8);
+}
+
 // Persistent warps; each warp repeatedly claims the next slot (atomic ticket)
 // and streams it: coalesced 128-bit loads of lp/old/ref (+adv) and 32-bit
 // mask words, kUnroll vectors per lane in flight, fused advantage broadcast,
@@ -306,14 +360,10 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     }
   }
 
-  float mu = 0.0f, rstd = 1.0f;
-  if (p.whiten) {
-    const double N = p.whiten_sums[2];
-    const double m1 = N > 0 ? p.whiten_sums[0] / N : 0.0;
-    const double var = N > 1 ? (p.whiten_sums[1] - p.whiten_sums[0] * m1) / (N - 1.0) : 0.0;
-    mu = (float)m1;
-    rstd = (float)(1.0 / sqrt(fmax(var, 0.0) + 1e-8));
-  }
+  // whitening coefficients: live across the loop only for per-token advantages; the per-rollout paths whiten
+  // once per slot (keeps the hot kernels' registers for loads in flight)
+  double mu = 0.0, rstd = 1.0;
+  if (ADV == DFX_ADV_TOKEN && p.whiten) whiten_coeffs(p, mu, rstd);
   double* part = p.part;
   // tickets: [k] next slot of source k, [kMaxLossSrc] finished warps. Several sources (e.g. local HBM and a
   // partner GPU's memory over NVLink) are drained concurrently: warp w starts on source w % n_src and moves to the
@@ -351,8 +401,12 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     } else if (ADV == DFX_ADV_ROLLOUT) {
       A_unit = (float)S.adv_roll_in[s];
     }
-    if (ADV != DFX_ADV_TOKEN) A_unit = (A_unit - mu) * rstd;  // identity unless whitening
-    const UnitAdv ua = unit_adv(A_unit, 1.0f - p.clip_lo, 1.0f + p.clip_hi);
+    if (ADV != DFX_ADV_TOKEN && p.whiten) {
+      double m0, r0;
+      whiten_coeffs(p, m0, r0);
+      A_unit = (float)(((double)A_unit - m0) * r0);
+    }
+    const UnitAdv ua = unit_adv(A_unit, 1.0f - p.clip_lo, 1.0f + p.clip_hi, p.t_lo32, p.t_hi32);
     float w = 0.0f;
     if (DLOGP) {
       int gi = 0;
@@ -720,13 +774,15 @@ inline int loss_variant() {
 
 template <int ADV, int KL, bool DL>
 void launch_slots(const LossParams& p, cudaStream_t st) {
-  if (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL && p.n_src > 1) {
-    // sources read over NVLink have ~2x the latency of local HBM: more vectors in flight per lane
-    static const int mu = std::getenv("DFX_LOSS_MULTI_UNROLL") ? std::atoi(std::getenv("DFX_LOSS_MULTI_UNROLL")) : 4;
-    if (mu == 4) return launch_variant<ADV, KL, DL, 4, 2>(p, st);
-    if (mu == 3) return launch_variant<ADV, KL, DL, 3, 2>(p, st);
-  }
-  if (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL) {
+  // (the tuning variants are instantiated for the hot configuration only)
+  if constexpr (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL) {
+    if (p.n_src > 1) {
+      // sources read over NVLink have ~2x the latency of local HBM: more vectors in flight per lane
+      static const int mu =
+          std::getenv("DFX_LOSS_MULTI_UNROLL") ? std::atoi(std::getenv("DFX_LOSS_MULTI_UNROLL")) : 4;
+      if (mu == 4) return launch_variant<ADV, KL, DL, 4, 2>(p, st);
+      if (mu == 3) return launch_variant<ADV, KL, DL, 3, 2>(p, st);
+    }
     switch (loss_variant()) {
       case 1: return launch_variant<ADV, KL, DL, 3, 2>(p, st);
       case 2: return launch_variant<ADV, KL, DL, 4, 2>(p, st);
@@ -736,7 +792,8 @@ void launch_slots(const LossParams& p, cudaStream_t st) {
       default: break;
     }
   }
-  launch_variant<ADV, KL, DL, 2, 3>(p, st);
+  // per-token advantages (GAE, f64 whitening) need more registers than the 80 of 3 CTAs/SM: 2 CTAs/SM
+  launch_variant<ADV, KL, DL, 2, ADV == DFX_ADV_TOKEN ? DFX_TOKEN_MINB : 3>(p, st);
 }
 
 template <int ADV, int KL>
@@ -910,6 +967,14 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
   p.whiten = cfg->whiten;
   p.clip_lo = (float)cfg->clip_low;
   p.clip_hi = (float)cfg->clip_high;
+  {
+    const double t_hi = std::log(1.0 + cfg->clip_high);
+    const double t_lo = cfg->clip_low < 1.0 ? std::log(1.0 - cfg->clip_low) : -HUGE_VAL;
+    p.t_hi32 = (float)t_hi;
+    p.t_lo32 = (float)t_lo;
+    p.t_hi32_lo = (float)(t_hi - (double)p.t_hi32);
+    p.t_lo32_lo = std::isfinite(t_lo) ? (float)(t_lo - (double)p.t_lo32) : 0.0f;
+  }
   p.beta = (float)cfg->beta;
   p.adv_eps = cfg->adv_eps;
   p.kl_type = cfg->kl_type;

@@ -177,13 +177,13 @@ def test_gae_long_rollouts_deterministic(O, dfx):
     db = dfx.PackedBatch.synthetic(5, 3, 1, dfx.TokenDist("constant", L, L, L), streams=streams)
     ctx = dfx.StageContext(gae_gamma=0.999, gae_lambda=0.99)
     outs = []
-    for _ in range(3):
+    T = sb.n_tokens
+    for _ in range(3):  # (the streams' padding past T is never written: compare the tokens)
         dfx.fn_gae_advantage(dfx.NodeSpec("g"), db, ctx)
-        outs.append((db.streams["advantage"].clone(), db.streams["returns"].clone(),
+        outs.append((db.streams["advantage"][:T].clone(), db.streams["returns"][:T].clone(),
                      db.channels["_whiten_sums"].clone()))
     for o in outs[1:]:
         assert all(torch.equal(x, y) for x, y in zip(o, outs[0]))
-    T = sb.n_tokens
     A, Rt, _ = O.gae(sb.cu_seqlens, sb.token_reward, sb.value_tok, sb.mask, 0.999, 0.99)
     assert_close_vec(outs[0][0][:T].cpu().numpy(), A[:T], "long gae adv")
     assert_close_vec(outs[0][1][:T].cpu().numpy(), Rt[:T], "long gae ret")
