@@ -66,6 +66,11 @@ def parse():
     ap.add_argument("--tp-read", action="store_true",
                     help="TP partners on different GPUs: every TP worker streams its whole group (the partner's half "
                          "over NVLink) instead of the default TP-split loss")
+    ap.add_argument("--store", default="native", choices=["native", "python"],
+                    help="c4: the native distributed DataBuffer (libdfx, one C call per verb, NCCL) or the Python "
+                         "DeviceBufferStore")
+    ap.add_argument("--transport", default="pull", choices=["pull", "nccl"],
+                    help="c4 native store: CUDA-IPC pulls by the copy engines (default) or NCCL send/recv")
     ap.add_argument("--placement", default="box", choices=["box", "store"],
                     help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
                          "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")
@@ -422,7 +427,9 @@ def run_c4(args):
     """BASELINE config 4: the inter-stage reshard round trip DP 8 -> 4 (tp 2) -> 8 of a 16.8M-token rollout batch
     (1024 prompts x 16 x 1024 tokens; payload token_id, lp, old_lp, ref_lp = 16 B/token, plus reward / advantage),
     one DataBuffer per GPU (B = N stores; logical world 8, or 16 at N = 8 where one worker per GPU cannot host a
-    tp-2 group), materialized consumer batches (get() semantics): copy-engine pulls over NVLink + unpack."""
+    tp-2 group), materialized consumer batches (get() semantics). Default: the native distributed DataBuffer
+    (libdfx dfx_dstore_*: one C call per verb, grouped NCCL send/recv straight between the producers' and the
+    consumers' streams, local copies overlapped); --store python: the Python store (CUDA-IPC pulls)."""
     import torch
     import torch.distributed as dist
 
@@ -435,60 +442,101 @@ def run_c4(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    native = args.store == "native"
     meta = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        meta = dist.new_group(backend="gloo")
+        dist.init_process_group("gloo" if native else "nccl", device_id=None if native else dev)
+        meta = None if native else dist.new_group(backend="gloo")
     logical = 16 if world == 8 else 8
     W = logical // world
     topo = Topology.box(logical, 1) if world == 1 else Topology.store_per_gpu(world, W)
     dp = logical
-    stages = {"s": StoreStagePlan(Layout(dp, 1), Layout(dp // 2, 2)), "t": StoreStagePlan(Layout(dp // 2, 2), Layout(dp, 1))}
-    store = DeviceBufferStore(topo, rank, stages, meta_group=meta)
+    to_s, to_t = Layout(dp // 2, 2), Layout(dp, 1)
+    stages = {"s": StoreStagePlan(Layout(dp, 1), to_s), "t": StoreStagePlan(to_s, to_t)}
     R = 1024 // world
     batch = dfx.PackedBatch.synthetic(11, R, 16, dfx.TokenDist("constant", 1024), device=dev, first_id=rank * R,
                                       streams=("token_id", "lp", "old_lp", "ref_lp"))
     dfx.fn_group_advantage(dfx.NodeSpec("a"), batch, dfx.StageContext())
     local_p = [p for p in range(dp) if topo.gpu_of_worker[p] == rank]
     per = R // len(local_p)
+    views = [batch.view_records(j * per, (j + 1) * per) for j in range(len(local_p))]
+    mine_s = [d for d in range(to_s.dp) if any(topo.gpu_of_worker[d * 2 + t] == rank for t in range(2))]
     it = [0]
-    moved = [0]
+    stream = torch.cuda.current_stream(dev)
+    if native:
+        from paper_2507_13833_b200.dstore import Comm, NativeBufferStore
+        comm = Comm.create(world, rank)
+        store = NativeBufferStore(topo, comm, stages, [("token_id", torch.int32), ("lp", torch.float32),
+                                                       ("old_lp", torch.float32), ("ref_lp", torch.float32)],
+                                  ["advantage", "reward"], stream=stream, transport=args.transport)
 
-    def step():
-        i = it[0]
-        for j, p in enumerate(local_p):
-            store.put("s", i, p, 0, batch.view_records(j * per, (j + 1) * per))
-        cb = store.ensure_ready("s", i, Layout(dp // 2, 2))
-        for k, d in enumerate(cb.groups):
-            for t in range(2):
-                if topo.gpu_of_worker[2 * d + t] == rank:
-                    store.put("t", i, d, t, cb.group_view(d))
-        cb2 = store.ensure_ready("t", i, Layout(dp, 1))
-        moved[0] = cb.bytes_recv + cb2.bytes_recv
-        for _ in store.local_workers:
-            store.worker_done(i)
-        it[0] += 1
+        # the C structs go straight through (no tensors are built for the consumer groups re-put into stage t)
+        from paper_2507_13833_b200.dstore import Batch
+        v_structs = [store.batch_struct(v) for v in views]
+        outs = {d: Batch() for d in mine_s}
+        puts_t = [(d, t) for d in mine_s for t in range(2) if topo.gpu_of_worker[d * 2 + t] == rank]
+        n_local = len(store.local_workers)
+
+        def step():
+            i = it[0]
+            for j, p in enumerate(local_p):
+                store.put_raw(b"s", i, p, 0, v_structs[j])
+            store.ensure_ready_raw(b"s", i, to_s)
+            for d in mine_s:
+                store.get_raw(b"s", i, d, to_s, outs[d])
+            for d, t in puts_t:
+                store.put_raw(b"t", i, d, t, outs[d])
+            store.ensure_ready_raw(b"t", i, to_t)
+            for _ in range(n_local):
+                store.worker_done_raw(i)
+            it[0] += 1
+
+        def moved():  # NVLink bytes this GPU received (pulled, or NCCL-received) = the peers' egress to it
+            st = store.stats()
+            return st["bytes_recv"]
+    else:
+        store = DeviceBufferStore(topo, rank, stages, meta_group=meta)
+
+        def step():
+            i = it[0]
+            for j, p in enumerate(local_p):
+                store.put("s", i, p, 0, views[j])
+            cb = store.ensure_ready("s", i, to_s)
+            for k, d in enumerate(cb.groups):
+                for t in range(2):
+                    if topo.gpu_of_worker[2 * d + t] == rank:
+                        store.put("t", i, d, t, cb.group_view(d))
+            store.ensure_ready("t", i, to_t)
+            for _ in store.local_workers:
+                store.worker_done(i)
+            it[0] += 1
+
+        def moved():
+            return store.bytes_sent
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     steps = max(1, args.steps)
+    m0 = moved()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        s0.record()
+        s0.record(stream)
         for _ in range(steps):
             step()
-        s1.record()
+        s1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     ms = s0.elapsed_time(s1) / steps
-    mv = float(moved[0])
+    mv = float(moved() - m0) / steps  # this GPU's NVLink egress per round trip
     if world > 1:
-        t = torch.tensor([ms, mv], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms, mv], dtype=torch.float64)
+        if not native:
+            t = t.to(dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, mv = float(t[0].item()), float(t[1].item())
     tokens = batch.token_span * world
@@ -501,11 +549,13 @@ def run_c4(args):
                 "config": {"workload": f"C4: DataBuffer round trip dp{dp} -> dp{dp // 2} (tp2) -> dp{dp} of 1024 "
                                        f"prompts x 16 x 1024 tokens (16.8M tokens, 16 B/token payload) over {world} GPU",
                            "placement": f"one DataBuffer per GPU (B={topo.num_nodes}, W={topo.workers_per_node})",
+                           "store": (f"native: libdfx dfx_dstore_* (C ABI), transport {args.transport}" if native
+                                     else "python: DeviceBufferStore (CUDA-IPC pulls)"),
                            "materialized": True, "global_tokens": tokens},
-                "e2e": None, "gpu_launches": 2 * 2,
+                "e2e": None, "gpu_launches": None,
                 "roofline": {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                              "frac": round(ach / NVLINK_PEER_GBS, 4), "traffic": None,
-                             "kernel": "the whole round trip (copy-engine pulls + unpack_kernel)",
+                             "kernel": "the whole round trip: per-GPU NVLink egress / step time",
                              "bytes_per_step_max_gpu": int(mv),
                              "peak_source": "measured peer copy, 770 GB/s per direction (B200_PROFILING.md)"},
                 "cpu_baseline": None, "clocks": clk.result()}

@@ -406,6 +406,10 @@ typedef struct dfx_batch {
   const int64_t* h_cu;
 } dfx_batch;
 
+/* Transports of remote segments: PULL maps the producers' allocations (CUDA IPC)
+ * and the consumer's copy engines read them over NVLink; NCCL posts one grouped
+ * ncclSend/ncclRecv per exchange (the library baseline, ~2.5x slower here). */
+enum { DFX_TRANSPORT_PULL = 0, DFX_TRANSPORT_NCCL = 1 };
 typedef struct dfx_dstore_cfg {
   uint32_t num_nodes, workers_per_node;  /* the reference's B x W logical world (topology.hpp:11-35) */
   const int32_t* rank_of_worker;         /* [B*W]: the process (GPU) rank hosting each logical worker */
@@ -418,6 +422,7 @@ typedef struct dfx_dstore_cfg {
   const uint32_t* produced_tp;
   const uint32_t* consumed_dp;           /* 0: the layout is given to ensure_ready (fallback_to_layout) */
   const uint32_t* consumed_tp;
+  int32_t transport;                     /* DFX_TRANSPORT_PULL (default) or DFX_TRANSPORT_NCCL */
 } dfx_dstore_cfg;
 typedef struct dfx_dstore dfx_dstore;
 
@@ -433,12 +438,13 @@ dfx_status dfx_dstore_put(dfx_dstore* s, const char* stage, uint64_t iteration, 
                           const dfx_batch* batch, int32_t* accepted);
 /* BufferStore::ensure_ready / exchange (:296-346, :400-442), collective over
  * the communicator: one all-reduce of the producer sizes (cached plan when they
- * repeat), then the reshard on the stream -- metadata pack kernel, ONE grouped
- * NCCL send/recv of every cross-GPU segment (token streams straight from the
- * producer's streams into the consumer's, 16-byte aligned or staged), local
- * segments by one copy kernel on a forked stream, one unpack kernel. Consumer
- * groups that are one contiguous local run are zero-copy views. DFX_NOT_READY
- * if a local producer group has not put. */
+ * repeat; the producers' IPC handles travel only when their memory changed),
+ * then the reshard on the stream -- remote token runs pulled by the copy
+ * engines over NVLink (or NCCL send/recv), local segments by one copy kernel on
+ * a forked stream, one unpack kernel. Consumer groups that are one contiguous
+ * run of local producer memory are zero-copy views. DFX_NOT_READY if a local
+ * producer group has not put. Put batches must stay unmodified until
+ * worker_done retires the iteration (peers may read them until then). */
 dfx_status dfx_dstore_ensure_ready(dfx_dstore* s, const char* stage, uint64_t iteration, uint32_t to_dp,
                                    uint32_t to_tp);
 /* BufferStore::get (:269-292): consumer group dest_dp's batch on this GPU (TP

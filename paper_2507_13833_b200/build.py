@@ -56,9 +56,8 @@ def build(verbose: bool = False) -> str:
             if log:
                 sys.stderr.write(log)
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        # NCCL (the distributed DataBuffer, csrc/dstore.cu): the system libnccl.so.2; inside a torch process the
-        # already-loaded libnccl.so.2 (same soname) serves it
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lnccl"]
+        # NCCL (csrc/dstore.cu) is dlopen'ed at run time by soname, not linked
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

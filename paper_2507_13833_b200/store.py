@@ -54,8 +54,9 @@ class _Entry:
 
 class DeviceBufferStore:
     def __init__(self, topo: Topology, rank: int, stages: dict, group=None, stream=None, meta_group=None,
-                 transport: str = "pull"):
+                 transport: str = "pull", schema=None):
         self.topo, self.rank, self.stages, self.group, self.stream = topo, rank, dict(stages), group, stream
+        self.schema = schema  # ({stream: dtype}, [channels]): needed on ranks that hold no producer group
         self.transport = transport  # "pull" (NVLink peer pulls) or "nccl" (grouped send/recv)
         self.meta_group = meta_group  # CPU (gloo) group for host metadata; data moves over `group` (NCCL)
         self.local_workers = [w for w in range(topo.world) if topo.gpu_of_worker[w] == rank]
@@ -130,9 +131,9 @@ class DeviceBufferStore:
                        else reuse_lazy(prev, self.group))
             self.template_hits += 1
         else:
-            e.ready = exchange(plan, sources, stream=self.stream, group=self.group, meta_group=self.meta_group,
-                               transport=self.transport, lazy=lazy, templates=self._mat_templates,
-                               template_key=tkey)
+            e.ready = exchange(plan, sources, stream=self.stream, group=self.group, schema=self.schema,
+                               meta_group=self.meta_group, transport=self.transport, lazy=lazy,
+                               templates=self._mat_templates, template_key=tkey)
             if lazy:
                 if tmpl is not None:
                     self._retired.append(tmpl[1])  # its mappings close once this iteration retires

@@ -34,7 +34,10 @@ meta = dist.new_group(backend="gloo")
 R, n, seed = 64, 4, 21
 dp_p, dp_c = world // 2, world
 topo = Topology.box(world, world)
-store = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(Layout(dp_p, 2), Layout(dp_c, 1))}, meta_group=meta)
+schema = ({"lp": torch.float32, "old_lp": torch.float32, "ref_lp": torch.float32, "mask": torch.uint8},
+          ["reward", "value", "advantage"])  # odd GPUs hold no producer group
+store = DeviceBufferStore(topo, rank, {"s": StoreStagePlan(Layout(dp_p, 2), Layout(dp_c, 1))}, meta_group=meta,
+                          schema=schema)
 p_mine = rank // 2 if rank % 2 == 0 else None  # producer group led by this GPU's worker (tp 0), if any
 b = None
 if p_mine is not None:
@@ -90,7 +93,8 @@ for it in range(10, 13):
     cb = store.ensure_ready("s", it, Layout(dp_c, 1), lazy=True)
     store.worker_done(it)
     torch.cuda.synchronize()
-    assert L.dfx_ipc_open_count() == opened, (rank, it, L.dfx_ipc_open_count(), opened)
+    live = set(store._templates["s"][1].ipc_bases or [])  # the mappings the current template may replay
+    assert L.dfx_ipc_open_count() == len(live), (rank, it, L.dfx_ipc_open_count(), len(live))
 dist.barrier()
 print(f"rank {rank}: loss {results and np.frombuffer(results[0])[0]:.9f} == oracle {want['loss']:.9f}; "
       f"mappings {opened} -> {L.dfx_ipc_open_count()}", flush=True)

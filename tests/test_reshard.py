@@ -245,6 +245,24 @@ def test_two_gpu_lazy_reshard_fused_loss():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n_gpus", [1, 2, 4])
+def test_native_dstore_blobs(n_gpus):
+    """The native distributed DataBuffer (libdfx dfx_dstore_*: one process per GPU, NCCL) reproduces the reference
+    BufferStore's destination blobs byte for byte, and the round trip gives back the producers' records
+    (tests/mp/dstore_worker.py)."""
+    if torch.cuda.device_count() < n_gpus:
+        pytest.skip(f"needs {n_gpus} GPUs")
+    port = 27600 + n_gpus * 50 + (os.getpid() % 40)
+    r = subprocess.run(["timeout", "300", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n_gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "mp", "dstore_worker.py")],
+                       capture_output=True, text=True, timeout=360, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("DSTORE_OK") == n_gpus, r.stdout[-2000:]
+    print(r.stdout[-1500:])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n_gpus", [2, 4])
 def test_mixed_zero_copy_lazy_reshard(n_gpus):
     """Zero-copy and peer-reading GPUs in one lazy reshard, several iterations over the same producer batches and a
@@ -257,7 +275,8 @@ def test_mixed_zero_copy_lazy_reshard(n_gpus):
                         f"--nproc-per-node={n_gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
                         os.path.join(ROOT, "tests", "mp", "mixed_lazy_worker.py")],
                        capture_output=True, text=True, timeout=360, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    errs = "\n".join(l for l in r.stderr.splitlines() if "Error" in l or "assert" in l)[-4000:]
+    assert r.returncode == 0, r.stdout[-2000:] + errs
     assert r.stdout.count("MIXED_OK") == n_gpus, r.stdout[-2000:]
     print(r.stdout[-1500:])
 

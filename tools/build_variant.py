@@ -41,7 +41,7 @@ def main():
     with cf.ThreadPoolExecutor(8) as ex:
         objs = list(ex.map(comp, B.sources()))
     lib = os.path.join(a.out, "libdfx.so")
-    subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-lnccl"], check=True)
+    subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-ldl"], check=True)
     print(lib)
 
 
