@@ -14,8 +14,8 @@ Workload per GPU: C2 = 1024 prompts x n=16 x UNIFORM[1,4096] tokens (~33.5M toke
 than L2, so no flush is needed between steps). Weak scaling: every rank holds its own C2 batch.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref: fn_group_advantage + BufferStore
-put/redistribute/get, compiled from /root/reference) plus the oracle's loss port (the reference has no loss) on a
-bounded sample, on this host's cores.
+put/redistribute/get, compiled from /root/reference) plus the oracle's loss port (the reference has no loss) on the
+same full C2 batch and step counts, on this host's cores.
 """
 from __future__ import annotations
 
@@ -63,9 +63,11 @@ def parse():
     ap.add_argument("--materialize", action="store_true",
                     help="copy remote records into a local consumer batch before the loss (default: the loss kernel "
                          "reads them in place over NVLink)")
-    ap.add_argument("--tp-read", action="store_true",
-                    help="TP partners on different GPUs: every TP worker streams its whole group (the partner's half "
-                         "over NVLink) instead of the default TP-split loss")
+    ap.add_argument("--tp-split", action="store_true",
+                    help="TP partners on different GPUs (N=8 box placement): instead of every TP worker consuming its "
+                         "whole consumer group (the partner's half read over NVLink by the loss kernel, the default), "
+                         "each streams only the rollouts it holds and the pair folds its loss rows -- a LOSS-ONLY "
+                         "figure: no token of the group reaches the other TP worker")
     ap.add_argument("--store", default="native", choices=["native", "python"],
                     help="c4: the native distributed DataBuffer (libdfx, one C call per verb, NCCL) or the Python "
                          "DeviceBufferStore")
@@ -247,9 +249,9 @@ class DagSlice:
             mode = ("records cross GPUs (dense slice/exchange/concat): each consumer maps the remote slices (CUDA "
                     "IPC) and the loss kernel streams them over NVLink in place (dfx_ppo_loss_multi), no copy")
         elif self.lazy and self.tp_group is not None:
-            mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC, the "
-                    "consumer's view of the group); TP-split loss: each TP worker streams the rollouts it holds and "
-                    "the pair folds its loss rows (56 B all-gather + dfx_loss_combine), no token crosses NVLink")
+            mode = ("LOSS-ONLY FIGURE (--tp-split): TP partners on different GPUs; each TP worker streams only the "
+                    "rollouts it holds and the pair folds its loss rows (56 B all-gather + dfx_loss_combine); no "
+                    "token of a consumer group reaches its other TP worker, so this is not a reshard measurement")
         elif self.lazy:
             mode = ("TP partners on different GPUs: each GPU maps its partner's producer group (CUDA IPC) and the "
                     "loss kernel streams it over NVLink in place (dfx_ppo_loss_multi), no copy")
@@ -298,7 +300,7 @@ def run_dfx(args):
     ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
     stream = torch.cuda.current_stream(dev)
     resh = DagSlice(dfx, world, rank, R, ctx, Layout, Topology, DeviceBufferStore, StoreStagePlan, args.placement,
-                    args.workers, lazy=not args.materialize, dev=dev, tp_split=not args.tp_read)
+                    args.workers, lazy=not args.materialize, dev=dev, tp_split=args.tp_split)
 
     ev0, ev1 = C.c_void_p(), C.c_void_p()
     _abi.check(L.dfx_event_create(C.byref(ev0)))
@@ -616,12 +618,10 @@ def run_e2e(args, dfx, batch, ctx, resh, dev, stream, world):
 
 
 # ---- CPU arm: the reference's own code (oracle/_ref) + the oracle loss port -------------------
-CPU_SAMPLE_RECORDS = 64
-
-
-def cpu_sample():
+def cpu_sample(records=None):
+    """The CPU arm's batch: the GPU arm's own C2 workload (all 1024 prompts unless `records` says otherwise)."""
     from oracle import oracle as O
-    sb = O.SynthBatch(C2["seed"], CPU_SAMPLE_RECORDS, C2["n_roll"], O.token_dist("uniform", 0, 1, 4096),
+    sb = O.SynthBatch(C2["seed"], records or C2["records"], C2["n_roll"], O.token_dist(*C2["dist"]),
                       streams=("lp", "old_lp", "ref_lp", "mask", "token_id"))
     return O, sb
 
@@ -634,15 +634,19 @@ def cpu_step(O, sb, nthreads):
     on records whose payload is the 16 B/token streams (token id, lp, old, ref), then the loss port."""
     T = sb.n_tokens
     streams = [sb.token_id[:T], sb.lp[:T], sb.old_lp[:T], sb.ref_lp[:T]]
-    t0 = time.perf_counter()
     adv_s, rs_s = O.ref_bench(sb, streams, 1, 8, 8, 1, 4, 2, nthreads, 1)
-    t1 = time.perf_counter()
     adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
     adv_tok = O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask)
     t2 = time.perf_counter()
     O.ppo_loss_mt(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, adv_tok, sb.mask, O.loss_cfg(), LOSS_THREADS)
     t3 = time.perf_counter()
     return adv_s + rs_s + (t3 - t2), {"advantage_s": adv_s, "reshard_s": rs_s, "loss_port_s": t3 - t2}
+
+
+def _sample_text(sb, nthreads):
+    return (f"the full C2 batch ({sb.n_records} prompts x 16 x UNIFORM[1,4096] = {sb.n_tokens} tokens): reference "
+            f"fn_group_advantage + BufferStore dp8->dp4 (B=1, W=8; {nthreads} worker threads, runner.hpp:525-530) + "
+            f"the oracle's loss port ({LOSS_THREADS} threads, sequences split; the reference has no loss)")
 
 
 def cpu_baseline(records):
@@ -652,37 +656,37 @@ def cpu_baseline(records):
     ts = [cpu_step(O, sb, nthreads)[0] for _ in range(2)]
     t = min(ts)
     return {"value": round(sb.n_tokens / t, 1), "unit": UNIT, "cores": max(nthreads, LOSS_THREADS), "kind": "reference",
-            "sample": f"{CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096] ({sb.n_tokens} tokens, 1/16 of C2): "
-                      "reference fn_group_advantage + BufferStore dp8->dp4 (B=1,W=8; 8 worker threads) "
-                      f"+ oracle loss port ({LOSS_THREADS} threads, sequences split; the reference has no loss)",
-            "host_cpus": os.cpu_count()}
+            "sample": _sample_text(sb, nthreads), "host_cpus": os.cpu_count()}
 
 
 def run_reference(args):
+    """The reference's own CPU path on this host's cores, on the GPU arm's workload (full C2 per step) and step
+    counts (--steps / --warmup honoured); rank 0 alone under torchrun."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     O, sb = cpu_sample()
     nthreads = 8
-    for _ in range(max(args.warmup, 1)):
+    warm = max(args.warmup, 1)
+    for _ in range(warm):
         cpu_step(O, sb, nthreads)
-    steps = max(1, min(args.steps, 10))
+    steps = max(1, args.steps)
     ts, parts = [], None
     for _ in range(steps):
         t, parts = cpu_step(O, sb, nthreads)
         ts.append(t)
     t = sum(ts) / len(ts)
     v = round(sb.n_tokens / t, 1)
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": max(args.warmup, 1),
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (keyed SplitMix64)", "impl": "reference",
-            "config": {"workload": f"bounded sample of C2: {CPU_SAMPLE_RECORDS} prompts x 16 x UNIFORM[1,4096]",
-                       "tokens": sb.n_tokens, "phases_s": parts},
+            "config": {"workload": f"C2 per GPU: {sb.n_records} prompts x n=16 x UNIFORM[1,4096] tokens "
+                                   f"(~{sb.n_tokens / 1e6:.1f}M tokens), GRPO adv -> DataBuffer reshard (dp8 -> dp4, "
+                                   "tp 2) -> clipped loss + k3 KL token-mean", "tokens": sb.n_tokens,
+                       "phases_s": parts},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": max(nthreads, LOSS_THREADS), "kind": "reference",
-                             "sample": f"{sb.n_tokens} tokens; reference fn_group_advantage + BufferStore reshard "
-                                       "(oracle/_ref, compiled from /root/reference; 8 worker threads) + oracle loss port "
-                                       f"({LOSS_THREADS} threads)"},
+                             "sample": _sample_text(sb, nthreads)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
