@@ -129,6 +129,21 @@ size_t dfx_gae_workspace_bytes(int64_t n_rollouts, int64_t token_span);
 dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
                    float* adv, float* ret, double* whiten, void* workspace, size_t ws_bytes, dfx_stream stream);
 
+/* GAE fused with the PPO loss (new): one scan pass computes every token's
+ * advantage and, from it, the clipped surrogate + KL terms -- the advantage
+ * never goes to HBM (adv may be NULL; ret is written for the critic). Token-
+ * mean aggregation of unwhitened advantages only (cfg->agg ==
+ * DFX_AGG_TOKEN_MEAN, cfg->whiten == 0: whitening needs the global advantage
+ * statistics first -- use dfx_gae then dfx_ppo_loss). Same numerics as
+ * dfx_gae followed by dfx_ppo_loss with DFX_ADV_TOKEN, deterministic.
+ * Workspace zero-filled once at allocation (as dfx_gae's). */
+typedef struct dfx_loss_cfg dfx_loss_cfg;
+typedef struct dfx_loss_out dfx_loss_out;
+size_t dfx_gae_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span);
+dfx_status dfx_gae_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
+                            const dfx_loss_cfg* cfg, float* ret, float* adv, dfx_loss_out* out, void* workspace,
+                            size_t ws_bytes, dfx_stream stream);
+
 /* ---------------------------------------------------------------------------
  * PPO / GRPO clipped surrogate + KL + masked aggregation (new; fills the
  * fn_train slot, distflow/functions.hpp:176-182, node actor_train dag.hpp:335)

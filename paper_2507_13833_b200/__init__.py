@@ -10,7 +10,7 @@ from ._abi import lib as _lib
 _lib()  # fail loudly at import when the CUDA library is absent
 
 from .functions import (FunctionRegistry, LossConfig, NodeSpec, StageContext, builtin_gpu_registry,  # noqa: E402,F401
-                        fn_gae_advantage, fn_group_advantage, fn_ppo_advantage, fn_train, invoke_node, loss_dict,
+                        fn_gae_advantage, fn_group_advantage, gae_ppo_loss, fn_ppo_advantage, fn_train, invoke_node, loss_dict,
                         ppo_loss, ppo_loss_sources, preset_dag, registry_bind, reward_stats, aggregate_metrics,
                         tp_combine_loss)
 from .packed import PackedBatch  # noqa: E402,F401

@@ -72,6 +72,9 @@ def _declare(L):
     L.dfx_gae_workspace_bytes.restype = sz
     L.dfx_gae_workspace_bytes.argtypes = [i64, i64]
     L.dfx_gae.argtypes = [C.POINTER(Packed), i64, i64, f64, f64, P, P, P, P, sz, P]
+    L.dfx_gae_ppo_loss_workspace_bytes.restype = sz
+    L.dfx_gae_ppo_loss_workspace_bytes.argtypes = [i64, i64]
+    L.dfx_gae_ppo_loss.argtypes = [C.POINTER(Packed), i64, i64, f64, f64, C.POINTER(LossCfg), P, P, P, P, sz, P]
     L.dfx_ppo_loss_workspace_bytes.restype = sz
     L.dfx_ppo_loss_workspace_bytes.argtypes = [i64, i64, i32]
     L.dfx_ppo_loss.argtypes = [C.POINTER(Packed), i64, i64, C.POINTER(LossCfg), C.POINTER(LossArgs), P, sz, P]
@@ -89,6 +92,7 @@ def _declare(L):
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     for name in ("dfx_grpo_advantage", "dfx_broadcast_advantage", "dfx_ppo_advantage", "dfx_gae", "dfx_ppo_loss",
+                 "dfx_gae_ppo_loss",
                  "dfx_ppo_loss_multi",
                  "dfx_check_flags", "dfx_synth_tokens", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
                  "dfx_event_elapsed_ms"):

@@ -115,6 +115,29 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- per-token loss math shared by the loss kernels (loss.cu) and the fused GAE + loss scan (gae.cu) ---------
+// k3 = e^x - x - 1 (x = ref - lp) by its Taylor series for |x| < 1/8 (truncation < 1.2e-8 relative); callers
+// fall back to expm1f(x) - x, which has no cancellation, for larger |x|.
+__device__ __forceinline__ float k3_series(float x) {
+  float q = 1.0f / 720.0f;
+  q = fmaf(q, x, 1.0f / 120.0f);
+  q = fmaf(q, x, 1.0f / 24.0f);
+  q = fmaf(q, x, 1.0f / 6.0f);
+  q = fmaf(q, x, 0.5f);
+  return (x * x) * q;
+}
+constexpr float kK3Series = 0.125f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Exact clip decision s*(l - o) > s*T for f32 inputs l, o (d = f32(l - o)) against a threshold given as the float
+// pair sT32 + sTl (= s*T to ~2^-48): TwoSum gives d + e == l - o exactly, and s*d - sT32 is exact wherever the sign
+// of the total is in doubt (Sterbenz). sT32 = +inf: never.
+__device__ __forceinline__ bool clip_exact_f32(float s, float sT32, float sTl, float l, float o, float d) {
+  const float bb = d - l;
+  const float e = (l - (d - bb)) + (-o - bb);
+  return (s * d - sT32) + (s * e - sTl) > 0.0f;
+}
+
 // ---- reference hash (distflow/hash.hpp), integer-exact on device ------------
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

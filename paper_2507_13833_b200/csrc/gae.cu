@@ -25,6 +25,7 @@
 // Arithmetic: f32 inputs and outputs; deltas, chunk maps, scans and the per-token recurrence in f64. HBM-bound:
 // 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map. Design history: profiles/r01_gae_experiments.md.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
@@ -51,6 +52,16 @@ struct GaeParams {
   ulonglong2* rec;                // [n_tiles] published tile state
   double* part;                   // [3][n_tiles] whitening partials
   uint8_t* ends;                  // bit (t - base): token t is the last token of its rollout; all-zero between calls
+  // fused GAE + PPO loss (dfx_gae_ppo_loss): the clipped surrogate + KL of every token from its advantage as the
+  // scan produces it -- the advantage never goes to HBM
+  const float* lp;
+  const float* old_lp;
+  const float* ref_lp;
+  float lo1, hi1;                 // 1 - eps_lo, 1 + eps_hi
+  float t_hi32, t_lo32, t_hi32_lo, t_lo32_lo;  // log-ratio thresholds as float pairs (clip_exact_f32)
+  int kl_type;
+  double* lpart;                  // [5][n_tiles] per-tile loss sums {pg, kl, approx_kl, clip, n}
+  uint8_t* seq_has;               // [n_seq] rollout has a masked token (prep), summed in order by the finish
 };
 
 struct Aff {
@@ -86,6 +97,42 @@ __global__ void __launch_bounds__(256) gae_prep_kernel(const int64_t* __restrict
   if (b <= a) return;  // empty rollouts own no token
   const int64_t e = b - 1 - base;
   atomicOr(ends + (e >> 5), 1u << (e & 31));
+}
+
+// fused variant: warp per rollout -- the end bit, the look-back epoch, and whether the rollout has a masked token
+// (the sequence count of the loss), found with 16-byte mask loads and an early exit
+__global__ void __launch_bounds__(256) gae_prep_loss_kernel(const int64_t* __restrict__ cu, int64_t n_seq,
+                                                            int64_t base, uint32_t* __restrict__ ends,
+                                                            unsigned long long* ticket,
+                                                            const uint8_t* __restrict__ mask, uint8_t* seq_has) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s == 0 && lane == 0) ticket[2] = (ticket[2] + 1ull) & 0x3fffffffull;
+  if (s >= n_seq) return;
+  const int64_t a = __ldg(cu + s), b = __ldg(cu + s + 1);
+  bool has = false;
+  if (b > a) {
+    if (lane == 0) {
+      const int64_t e = b - 1 - base;
+      atomicOr(ends + (e >> 5), 1u << (e & 31));
+    }
+    for (int64_t t0 = a & ~int64_t(15); t0 < b && !has; t0 += 512) {
+      const int64_t t = t0 + 16 * lane;
+      uint32_t any = 0;
+      if (t < b) {
+        const uint4 v = *reinterpret_cast<const uint4*>(mask + t);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t tq = t + q;
+          if (tq >= a && tq < b && ((w[q >> 2] >> (8 * (q & 3))) & 0xffu)) any = 1;
+        }
+      }
+      has = __any_sync(kFull, any);
+    }
+  }
+  if (lane == 0) seq_has[s] = has ? 1 : 0;
 }
 
 // ---- the scan ---------------------------------------------------------------------------------------------------
@@ -150,9 +197,17 @@ template <int THREADS>
 struct SmemTile {
   static constexpr int TILE = THREADS * 32;
   static constexpr uint32_t kR = 0, kV = TILE * 4 + 16, kM = 2 * (TILE * 4 + 16), kBytes = kM + TILE + 16;
+  // fused loss: lp, old, ref of the tile after the mask
+  static constexpr uint32_t kL = (kBytes + 127) & ~127u, kO = kL + TILE * 4, kF = kO + TILE * 4,
+                            kBytesLoss = kF + TILE * 4;
 };
 
-template <int THREADS, int MINB, bool WHITEN>
+#ifndef DFX_GAE_LOSS_SMEM
+#define DFX_GAE_LOSS_SMEM 0  // fused loss inputs: 0 = L2 prefetch + per-thread loads, 1 = TMA into shared memory
+#endif
+constexpr bool kLossSmem = DFX_GAE_LOSS_SMEM != 0;
+
+template <int THREADS, int MINB, bool WHITEN, bool LOSS = false>
 __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   using L = SmemTile<THREADS>;
   constexpr int TILE = L::TILE, NW = THREADS / 32;
@@ -163,7 +218,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ Aff s_warp[NW];
   __shared__ double s_X;
-  __shared__ double s_red[NW][3];
+  __shared__ double s_red[NW][LOSS ? 5 : 3];
+  const float* s_l = reinterpret_cast<const float*>(sm + L::kL);
+  const float* s_o = reinterpret_cast<const float*>(sm + L::kO);
+  const float* s_f = reinterpret_cast<const float*>(sm + L::kF);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t tile = p.n_tiles - 1 - (int64_t)blockIdx.x;
   const int64_t T0 = p.base + tile * TILE;
@@ -175,10 +233,19 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     mbar_fence_init();
-    mbar_arrive_expect_tx(&s_bar, 9u * n);
+    mbar_arrive_expect_tx(&s_bar, (LOSS && kLossSmem ? 21u : 9u) * n);
     tma_load_1d(s_r, p.rew + T0, 4u * n, &s_bar);
     tma_load_1d(s_v, p.val + T0, 4u * n, &s_bar);
     tma_load_1d(s_m, p.mask + T0, n, &s_bar);
+    if (LOSS && kLossSmem) {
+      tma_load_1d(sm + L::kL, p.lp + T0, 4u * n, &s_bar);
+      tma_load_1d(sm + L::kO, p.old_lp + T0, 4u * n, &s_bar);
+      tma_load_1d(sm + L::kF, p.ref_lp + T0, 4u * n, &s_bar);
+    } else if (LOSS) {  // into L2 now, read per thread in pass 2 (keeps shared memory -- and occupancy -- as GAE's)
+      l2_prefetch(p.lp + T0, 4u * n);
+      l2_prefetch(p.old_lp + T0, 4u * n);
+      l2_prefetch(p.ref_lp + T0, 4u * n);
+    }
     // the token after the tile (V, mask) sits one past the tile in shared memory
     const int64_t tn = T0 + TILE;
     s_v[TILE] = tn < p.end ? __ldg(p.val + tn) : 0.0f;
@@ -289,6 +356,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   const double Xin = fma(E.c, Xd, E.d);
   double X = fma(Tc, Xin, Td);
   float wa = 0.0f, wa2 = 0.0f;
+  float lpg = 0.0f, lkl = 0.0f, lakl = 0.0f, lclip = 0.0f;  // fused loss sums over this thread's tokens
   float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
   int pend_i = -1;
 #pragma unroll
@@ -301,6 +369,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
     if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
     const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), o4 = l4, f4 = l4;
+    if (LOSS && !kLossSmem && T0 + tid * 32 + ch * 4 + 4 <= rd_end) {  // (L2 hits: prefetched at the start)
+      const int64_t g = T0 + tid * 32 + ch * 4;
+      l4 = *reinterpret_cast<const float4*>(p.lp + g);
+      o4 = *reinterpret_cast<const float4*>(p.old_lp + g);
+      f4 = *reinterpret_cast<const float4*>(p.ref_lp + g);
+    }
     float oa[4], orr[4];
 #pragma unroll
     for (int k = 3; k >= 0; --k) {
@@ -317,6 +392,25 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
         wa = fmaf(mw, oa[k], wa);
         wa2 = fmaf(mw * oa[k], oa[k], wa2);
       }
+      if (LOSS && (((mbits & ~ident) >> q) & 1u)) {  // the PPO terms of a masked token (oracle dfo_ppo_loss)
+        const int i = i0 + k;
+        const float l = kLossSmem ? s_l[i] : f4_get(l4, k), o = kLossSmem ? s_o[i] : f4_get(o4, k),
+                    rf = kLossSmem ? s_f[i] : f4_get(f4, k), A = oa[k];
+        const float d = l - o;
+        const float rho = exp2f(d * kLog2e);
+        const float rc = fminf(fmaxf(rho, p.lo1), p.hi1);
+        lpg += fmaxf(-A * rho, -A * rc);
+        const float sg = A < 0.0f ? -1.0f : 1.0f;
+        const float sT = A > 0.0f ? p.t_hi32 : (A < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
+        lclip += clip_exact_f32(sg, sT, sg > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo, l, o, d) ? 1.0f : 0.0f;
+        const float x = rf - l;
+        float kl = 0.0f;
+        if (p.kl_type == DFX_KL_K3) kl = fabsf(x) < kK3Series ? k3_series(x) : fminf(fmaxf(expm1f(x) - x, -10.0f), 10.0f);
+        else if (p.kl_type == DFX_KL_K1) kl = -x;
+        else if (p.kl_type == DFX_KL_K2) kl = 0.5f * x * x;
+        lkl += kl;
+        lakl -= d;
+      }
     }
     if (interior) {
       *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
@@ -326,7 +420,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (!((ident >> (ch * 4 + k)) & 1u)) {
-          p.adv[c0 + ch * 4 + k] = oa[k];
+          if (!LOSS || p.adv) p.adv[c0 + ch * 4 + k] = oa[k];
           p.ret[c0 + ch * 4 + k] = orr[k];
         }
       }
@@ -337,9 +431,22 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      tma_store_1d(p.adv + T0, s_r, 4u * TILE);
+      if (!LOSS || p.adv) tma_store_1d(p.adv + T0, s_r, 4u * TILE);  // (fused: the advantage stays on chip)
       tma_store_1d(p.ret + T0, s_v, 4u * TILE);
       tma_store_commit_and_wait();
+    }
+  }
+  if (LOSS) {  // per-tile loss sums: fixed-shape block reduction, summed over tiles in order by the finish kernel
+    const double v5[5] = {warp_sum((double)lpg), warp_sum((double)lkl), warp_sum((double)lakl),
+                          warp_sum((double)lclip), warp_sum((double)__popc(mbits & ~ident))};
+    if (lane == 0)
+      for (int q = 0; q < 5; ++q) s_red[wid][q] = v5[q];
+    __syncthreads();
+    if (tid < 5) {
+      double t5 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t5 += s_red[w][tid];
+      p.lpart[(int64_t)tid * p.n_tiles + tile] = t5;
     }
   }
   if (WHITEN) {
@@ -382,6 +489,40 @@ __global__ void __launch_bounds__(256) gae_finish_kernel(const double* __restric
   }
 }
 
+// fused loss: the per-tile sums in tile order (fixed-shape tree) -> token-mean dfx_loss_out; the sequence count
+// from the prep kernel's per-rollout flags
+__global__ void __launch_bounds__(256) gae_loss_finish_kernel(const double* __restrict__ lpart, int64_t n_tiles,
+                                                              const uint8_t* __restrict__ seq_has, int64_t n_seq,
+                                                              double beta, dfx_loss_out* out) {
+  __shared__ double s_red[8][6];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t i = tid; i < n_tiles; i += 256)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) tot[q] += lpart[(int64_t)q * n_tiles + i];
+  for (int64_t s = tid; s < n_seq; s += 256) tot[5] += seq_has[s] ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) tot[q] = warp_sum(tot[q]);
+  if (lane == 0)
+    for (int q = 0; q < 6; ++q) s_red[wid][q] = tot[q];
+  __syncthreads();
+  if (tid == 0) {
+    double t6[6] = {0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < 8; ++w)
+      for (int q = 0; q < 6; ++q) t6[q] += s_red[w][q];
+    const double N = t6[4];
+    dfx_loss_out o;
+    o.pg_loss = N > 0 ? t6[0] / N : 0.0;
+    o.kl = N > 0 ? t6[1] / N : 0.0;
+    o.loss = o.pg_loss + beta * o.kl;
+    o.approx_kl = N > 0 ? t6[2] / N : 0.0;
+    o.clipfrac = N > 0 ? t6[3] / N : 0.0;
+    o.n_tokens = N;
+    o.n_seqs = t6[5];
+    *out = o;
+  }
+}
+
 int64_t gae_tiles(int64_t token_base, int64_t token_span, int64_t tile) {
   const int64_t base = token_base & ~int64_t(15);
   return (token_base + token_span - base + tile - 1) / tile;
@@ -390,13 +531,14 @@ int64_t gae_tiles(int64_t token_base, int64_t token_span, int64_t tile) {
 constexpr int64_t kGaeMinTile = 2048;  // smallest tile of any variant (s64: 64 x 32 tokens; workspace sizing)
 
 struct GaeWs {
-  size_t ticket, ends, rec, part, bytes;
+  size_t ticket, ends, rec, part, lpart, bytes;
   int64_t cap_tiles;
 };
 // The layout is a function of the tile CAPACITY only, never of the call's span: the self-maintained state (the
 // epoch ticket and the all-zero end bitmap) must sit at the same offsets on every call that reuses a workspace, or
 // a call with a smaller span would OR its end bits onto a previous call's tile records / whitening partials.
-// Order: ticket, end bitmap (both kept consistent by the kernels), then the regions written before being read.
+// Order: ticket, end bitmap (both kept consistent by the kernels), then the regions written before being read;
+// the fused loss's per-rollout flags follow the capacity part (written before read as well).
 GaeWs gae_ws_layout_cap(int64_t cap_tiles) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   GaeWs w{};
@@ -405,14 +547,15 @@ GaeWs gae_ws_layout_cap(int64_t cap_tiles) {
   w.ends = al(3 * sizeof(unsigned long long));
   w.rec = w.ends + al(size_t(cap_tiles) * kGaeMinTile / 8 + 16);
   w.part = w.rec + al(16 * size_t(cap_tiles));
-  w.bytes = w.part + al(24 * size_t(cap_tiles));
+  w.lpart = w.part + al(24 * size_t(cap_tiles));
+  w.bytes = w.lpart + al(40 * size_t(cap_tiles));
   return w;
 }
 // tiles needed for a span (tile count depends on token_base & 15 as well: size for the worst case)
 int64_t gae_tiles_needed(int64_t token_span) { return (token_span + 15) / kGaeMinTile + 2; }
 // the largest capacity whose layout fits in ws_bytes (the caller's buffer size fixes the layout)
 GaeWs gae_ws_layout_fit(size_t ws_bytes) {
-  int64_t cap = (int64_t)(ws_bytes / (kGaeMinTile / 8 + 16 + 24));  // an upper bound; step down to the fit
+  int64_t cap = (int64_t)(ws_bytes / (kGaeMinTile / 8 + 16 + 24 + 40));  // an upper bound; step down to the fit
   while (cap > 0 && gae_ws_layout_cap(cap).bytes > ws_bytes) --cap;
   return gae_ws_layout_cap(cap);
 }
@@ -429,36 +572,37 @@ inline int gae_variant() {
   return v;
 }
 
-template <int THREADS, int MINB>
+template <int THREADS, int MINB, bool LOSS = false>
 void gae_launch_smem(GaeParams& p, cudaStream_t st) {
   using L = SmemTile<THREADS>;
+  constexpr uint32_t kSmem = LOSS && kLossSmem ? L::kBytesLoss : L::kBytes;
   p.n_tiles = gae_tiles(p.begin, p.end - p.begin, L::TILE);
   static thread_local int cached_dev = -1, resident = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev != cached_dev) {
     int sms = 0, per_sm = 0;
-    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
-    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
+    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, true, LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    cudaFuncSetAttribute(gae_smem_kernel<THREADS, MINB, false, LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_smem_kernel<THREADS, MINB, true>, THREADS, L::kBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_smem_kernel<THREADS, MINB, true, LOSS>, THREADS, kSmem);
     resident = sms * std::max(per_sm, 1);
     cached_dev = dev;
   }
   static const int pf_env = std::getenv("DFX_GAE_PF") ? std::atoi(std::getenv("DFX_GAE_PF")) : 100;
-  p.pf_dist = (int64_t)resident * pf_env / 100;
+  p.pf_dist = LOSS ? 0 : (int64_t)resident * pf_env / 100;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)p.n_tiles);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap launch + loads with gae_prep_kernel
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (p.whiten) cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, true>, p);
-  else cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, false>, p);
+  if (p.whiten) cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, true, LOSS>, p);
+  else cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, false, LOSS>, p);
 }
 
 
@@ -517,6 +661,77 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
     gae_finish_kernel<<<1, 256, 0, stream>>>(p.part, p.n_tiles, whiten);
     DFX_LAUNCH_CHECK("gae_finish_kernel");
   }
+  return DFX_OK;
+}
+
+
+// (the fused pass keeps its per-rollout flags in the whitening-partials region, 24 bytes per tile of capacity)
+size_t dfx_gae_ppo_loss_workspace_bytes(int64_t n_rollouts, int64_t token_span) {
+  return gae_ws_layout_cap(std::max(gae_tiles_needed(token_span), std::max<int64_t>(n_rollouts, 0) / 24 + 1)).bytes;
+}
+
+dfx_status dfx_gae_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
+                            const dfx_loss_cfg* cfg, float* ret, float* adv, dfx_loss_out* out, void* workspace,
+                            size_t ws_bytes, dfx_stream stream) {
+  if (!b || !cfg || !out || !ret || !b->cu_seqlens || !b->token_reward || !b->value_tok || !b->mask || !b->lp ||
+      !b->old_lp || !b->ref_lp)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_gae_ppo_loss: the batch needs cu_seqlens, token_reward, value_tok, mask, "
+                                      "lp, old_lp, ref_lp; ret and out are required");
+  if (cfg->agg != DFX_AGG_TOKEN_MEAN || cfg->whiten)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_gae_ppo_loss: the fused pass computes the token-mean loss of unwhitened "
+                                      "advantages (whitening or sequence means need dfx_gae + dfx_ppo_loss)");
+  if (cfg->kl_type < 0 || cfg->kl_type > 3) return fail(DFX_INVALID_ARGUMENT, "dfx_gae_ppo_loss: bad kl_type");
+  if (b->n_rollouts <= 0 || token_span <= 0) {
+    DFX_CUDA(cudaMemsetAsync(out, 0, sizeof(dfx_loss_out), stream));
+    return DFX_OK;
+  }
+  const GaeWs wl = gae_ws_layout_fit(ws_bytes);
+  if (!workspace || wl.cap_tiles < gae_tiles_needed(token_span) || 24 * wl.cap_tiles < b->n_rollouts)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_gae_ppo_loss: workspace too small");
+  char* w = static_cast<char*>(workspace);
+  GaeParams p{};
+  p.cu = b->cu_seqlens;
+  p.n_seq = b->n_rollouts;
+  p.begin = token_base;
+  p.end = token_base + token_span;
+  p.base = token_base & ~int64_t(15);
+  p.ticket = reinterpret_cast<unsigned long long*>(w + wl.ticket);
+  p.rec = reinterpret_cast<ulonglong2*>(w + wl.rec);
+  p.part = reinterpret_cast<double*>(w + wl.part);
+  p.ends = reinterpret_cast<uint8_t*>(w + wl.ends);
+  p.lpart = reinterpret_cast<double*>(w + wl.lpart);
+  p.seq_has = reinterpret_cast<uint8_t*>(w + wl.part);  // (no whitening here: the partials region is free)
+  p.rew = b->token_reward;
+  p.val = b->value_tok;
+  p.mask = b->mask;
+  p.gamma = gamma;
+  p.gl = gamma * lam;
+  p.adv = adv;
+  p.ret = ret;
+  p.whiten = nullptr;
+  p.lp = b->lp;
+  p.old_lp = b->old_lp;
+  p.ref_lp = b->ref_lp;
+  p.lo1 = 1.0f - (float)cfg->clip_low;
+  p.hi1 = 1.0f + (float)cfg->clip_high;
+  const double t_hi = std::log(1.0 + cfg->clip_high);
+  const double t_lo = cfg->clip_low < 1.0 ? std::log(1.0 - cfg->clip_low) : -HUGE_VAL;
+  p.t_hi32 = (float)t_hi;
+  p.t_lo32 = (float)t_lo;
+  p.t_hi32_lo = (float)(t_hi - (double)p.t_hi32);
+  p.t_lo32_lo = std::isfinite(t_lo) ? (float)(t_lo - (double)p.t_lo32) : 0.0f;
+  p.kl_type = cfg->kl_type;
+  gae_prep_loss_kernel<<<(unsigned)((p.n_seq + 7) / 8), 256, 0, stream>>>(
+      p.cu, p.n_seq, p.base, reinterpret_cast<uint32_t*>(p.ends), p.ticket, p.mask, p.seq_has);
+  DFX_LAUNCH_CHECK("gae_prep_loss_kernel");
+  switch (gae_variant()) {
+    case 1: gae_launch_smem<128, 4, true>(p, stream); break;
+    case 3: gae_launch_smem<64, 8, true>(p, stream); break;
+    default: gae_launch_smem<128, 5, true>(p, stream); break;
+  }
+  DFX_LAUNCH_CHECK("gae_smem_kernel<loss>");
+  gae_loss_finish_kernel<<<1, 256, 0, stream>>>(p.lpart, p.n_tiles, p.seq_has, p.n_seq, cfg->beta, out);
+  DFX_LAUNCH_CHECK("gae_loss_finish_kernel");
   return DFX_OK;
 }
 

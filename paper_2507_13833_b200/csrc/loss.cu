@@ -18,6 +18,9 @@
 #ifndef DFX_TOKEN_MINB
 #define DFX_TOKEN_MINB 2
 #endif
+#ifndef DFX_TOKEN_UNROLL
+#define DFX_TOKEN_UNROLL 2
+#endif
 
 namespace dfx {
 
@@ -143,21 +146,7 @@ struct LossParams {
   unsigned long long* ticket;  // [kMaxLossSrc + 1] per-source slot tickets + finished warps; zero on entry, restored
 };
 
-// ---- per-token math ---------------------------------------------------------
-// k3 = e^x - x - 1 (x = ref - lp) by its Taylor series for |x| < 1/8
-// (truncation < 1.2e-8 relative); callers fall back to expm1f(x) - x, which
-// has no cancellation, for the rare larger |x| (per vector, warp-uniform).
-__device__ __forceinline__ float k3_series(float x) {
-  float q = 1.0f / 720.0f;
-  q = fmaf(q, x, 1.0f / 120.0f);
-  q = fmaf(q, x, 1.0f / 24.0f);
-  q = fmaf(q, x, 1.0f / 6.0f);
-  q = fmaf(q, x, 0.5f);
-  return (x * x) * q;
-}
-constexpr float kK3Series = 0.125f;
-constexpr float kLog2e = 1.4426950408889634f;
-
+// ---- per-token math (k3_series, clip_exact_f32: common.cuh) ---------------------------------------------
 struct TokAcc {
   float pg, kl, akl, clip, n;
 };
@@ -184,15 +173,10 @@ __device__ __forceinline__ UnitAdv unit_adv(float A, float lo, float hi, float t
 
 // The clip fires iff s*(lp - old) > s*T, T the log-ratio threshold of A's sign (log(1+eps_hi) for A > 0,
 // log(1-eps_lo) for A < 0): the same decision as the reference formula's pg2 > pg1 on exp(lp - old) in f64
-// (oracle/dfx_oracle.c), made exactly in f32 arithmetic, branch-free: TwoSum gives d + e == lp - old exactly
-// (d = f32(lp - old)), the threshold is the float pair T32 + Tlo == T64 to ~2^-48, and s*d - s*T32 is exact
-// wherever the sign of the total is in doubt (Sterbenz), so the sum's sign is the exact comparison. Keeps clipfrac
-// (a count) exact instead of within f32 rounding of exp and 1+eps. A == 0: s*T32 = +inf, never clipped.
+// (oracle/dfx_oracle.c), made exactly in f32 arithmetic, branch-free (clip_exact_f32, common.cuh). Keeps clipfrac
+// (a count) exact instead of within f32 rounding of exp and 1+eps.
 __device__ __forceinline__ bool clip_twosum(const LossParams& p, float s, float sT32, float l, float o, float d) {
-  const float bb = d - l;
-  const float e = (l - (d - bb)) + (-o - bb);
-  const float sTl = s > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo;
-  return (s * d - sT32) + (s * e - sTl) > 0.0f;
+  return clip_exact_f32(s, sT32, s > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo, l, o, d);
 }
 
 // Four tokens of one aligned vector starting at token t. FULL: all in range.
@@ -793,7 +777,7 @@ void launch_slots(const LossParams& p, cudaStream_t st) {
     }
   }
   // per-token advantages (GAE, f64 whitening) need more registers than the 80 of 3 CTAs/SM: 2 CTAs/SM
-  launch_variant<ADV, KL, DL, 2, ADV == DFX_ADV_TOKEN ? DFX_TOKEN_MINB : 3>(p, st);
+  launch_variant<ADV, KL, DL, ADV == DFX_ADV_TOKEN ? DFX_TOKEN_UNROLL : 2, ADV == DFX_ADV_TOKEN ? DFX_TOKEN_MINB : 3>(p, st);
 }
 
 template <int ADV, int KL>

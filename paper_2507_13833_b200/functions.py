@@ -224,6 +224,38 @@ def fn_gae_advantage(node: NodeSpec, batch: PackedBatch, ctx: StageContext) -> N
 
 
 @_on_batch_device(0)
+def gae_ppo_loss(batch: PackedBatch, ctx: StageContext, want_adv: bool = False) -> dict:
+    """GAE fused with the PPO loss (dfx_gae_ppo_loss): one scan pass produces every token's advantage and its
+    clipped surrogate + KL terms; the advantage never goes to HBM (want_adv stores it too). Writes the 'returns'
+    stream (for the critic). Token-mean aggregation of unwhitened advantages; the two-pass path (fn_gae_advantage +
+    ppo_loss) covers whitening and sequence means. Returns {"out": [1, 7] device f64, ["adv"]}."""
+    cfg = ctx.loss
+    if cfg.whiten or cfg.agg != "token-mean":
+        raise errors.Error("gae_ppo_loss: the fused pass is token-mean over unwhitened advantages")
+    _require_rollouts(batch)
+    for n in ("token_reward", "value_tok", "mask", "lp", "old_lp", "ref_lp"):
+        _stream(batch, n)
+    like = batch.streams["token_reward"]
+    ret = torch.empty_like(like)
+    adv = torch.empty_like(like) if want_adv else None
+    out = torch.empty(7, dtype=torch.float64, device=batch.device)
+    c = _abi.LossCfg(cfg.clip_low, cfg.clip_high, cfg.beta, float(ctx.advantage_eps), _abi.KL[cfg.kl],
+                     _abi.AGG[cfg.agg], _abi.ADV["token"], 0)
+    L = _abi.lib()
+    nbytes = L.dfx_gae_ppo_loss_workspace_bytes(batch.n_rollouts, batch.token_span)
+    ws = ctx.workspace.get("gae_loss", nbytes, batch.device)
+    st = batch.struct()
+    _abi.check(L.dfx_gae_ppo_loss(C.byref(st), batch.token_base, batch.token_span, float(ctx.gae_gamma),
+                                  float(ctx.gae_lambda), C.byref(c), _ptr(ret), _ptr(adv), _ptr(out), _ptr(ws),
+                                  ws.numel(), ctx.cuda_stream(batch.device)))
+    batch.streams["returns"] = ret
+    res = {"out": out.view(1, 7)}
+    if adv is not None:
+        res["adv"] = adv
+    return res
+
+
+@_on_batch_device(0)
 def ppo_loss(batch: PackedBatch, ctx: StageContext, adv_source: str | None = None, loss_group_off=None,
              adv_tok_out: bool = False, events=None) -> dict:
     """Fused advantage + clipped surrogate + KL + masked aggregation. Returns device tensors.

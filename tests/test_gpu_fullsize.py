@@ -232,3 +232,44 @@ def test_multi_source_with_empty_source(dfx):
                                loss_group_off=[0, 128])["out"].cpu().numpy()[0]
     assert got[5] == whole[5] and got[6] == whole[6]
     np.testing.assert_allclose(got[:5], whole[:5], rtol=2e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("kl", ["k3", "k1", "none"])
+def test_c3_fused_gae_loss_full_size(O, dfx, kl):
+    """C3 (512 x 8192) through the fused GAE + loss pass (dfx_gae_ppo_loss): returns and the (optional) advantage
+    equal the two-pass path bit for bit, the loss scalars match the f64 oracle on the oracle's own GAE within 1e-5,
+    and two runs give the same bits."""
+    R, L = 512, 8192
+    streams = ("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward")
+    sb = O.SynthBatch(1, R, 1, O.token_dist("constant", L, L, L), streams=streams)
+    db = dfx.PackedBatch.synthetic(1, R, 1, dfx.TokenDist("constant", L, L, L), streams=streams)
+    ctx = dfx.StageContext(gae_gamma=1.0, gae_lambda=0.95)
+    ctx.loss = dfx.LossConfig(kl=kl, agg="token-mean")
+    T = sb.n_tokens
+    r1 = dfx.gae_ppo_loss(db, ctx, want_adv=True)
+    a1, ret1, o1 = r1["adv"][:T].clone(), db.streams["returns"][:T].clone(), r1["out"].clone()
+    r2 = dfx.gae_ppo_loss(db, ctx)
+    assert torch.equal(o1, r2["out"]) and torch.equal(ret1, db.streams["returns"][:T])
+    dfx.fn_gae_advantage(dfx.NodeSpec("g"), db, ctx)  # the two-pass path: same advantages and returns
+    assert torch.equal(a1, db.streams["advantage"][:T]) and torch.equal(ret1, db.streams["returns"][:T])
+    two = dfx.ppo_loss(db, ctx, adv_source="token")["out"].cpu().numpy()[0]
+    A, _, _ = O.gae(sb.cu_seqlens, sb.token_reward, sb.value_tok, sb.mask, 1.0, 0.95)
+    ref, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, A[:T].astype(np.float32), sb.mask,
+                        O.loss_cfg(kl=kl))
+    _check_loss(o1.cpu().numpy()[0], ref, f"C3 fused {kl}")
+    _check_loss(two, ref, f"C3 two-pass {kl}")
+
+
+def test_fused_gae_loss_ragged(O, dfx):
+    """The fused pass on ragged, skewed and empty rollouts and a view (token_base not tile-aligned)."""
+    streams = ("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward")
+    sb = O.SynthBatch(13, 40, 6, O.token_dist("skewed", 0, 0, 9000), streams=streams)
+    db = dfx.PackedBatch.synthetic(13, 40, 6, dfx.TokenDist("skewed", 0, 0, 9000), streams=streams)
+    ctx = dfx.StageContext(gae_gamma=0.99, gae_lambda=0.95)
+    v = db.view_records(3, 37)
+    s0, s1 = int(sb.group_off[3]), int(sb.group_off[37])
+    cu = np.ascontiguousarray(sb.cu_seqlens[s0:s1 + 1])
+    out = dfx.gae_ppo_loss(v, ctx)["out"].cpu().numpy()[0]
+    A, _, _ = O.gae(cu, sb.token_reward, sb.value_tok, sb.mask, 0.99, 0.95)
+    ref, _ = O.ppo_loss(cu, sb.lp, sb.old_lp, sb.ref_lp, A.astype(np.float32), sb.mask, O.loss_cfg())
+    _check_loss(out, ref, "fused ragged view")

@@ -121,6 +121,23 @@ def ppo_c3():
             "step": "GAE reverse scan (+whitening sums) -> whitened clipped surrogate + k3 KL token-mean"}
 
 
+def ppo_c3_fused():
+    """C3 through the fused GAE + loss pass (dfx_gae_ppo_loss): read r, V, mask, lp, old, ref (21 B/token), write
+    the returns (4 B/token); the advantage stays on chip. Token-mean, unwhitened (BASELINE config 3 names no
+    whitening)."""
+    b = dfx.PackedBatch.synthetic(1, 512, 1, dfx.TokenDist("constant", 8192),
+                                  streams=("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward"))
+    ctx = dfx.StageContext(gae_gamma=1.0, gae_lambda=0.95)
+    ctx.loss = dfx.LossConfig(kl="k3", agg="token-mean")
+    T = b.token_span
+    ms = graph_ms(lambda: dfx.gae_ppo_loss(b, ctx))
+    bytes_ = T * 25
+    return {"config": "C3 fused", "tokens": T, "step_graph_ms": ms, "tokens_per_s": T / (ms / 1e3),
+            "bytes_per_step": bytes_, "step_gbs": bytes_ / (ms / 1e3) / 1e9,
+            "step_frac_of_hbm": bytes_ / (ms / 1e3) / 1e9 / PEAK,
+            "step": "fused GAE reverse scan + clipped surrogate + k3 KL token-mean (dfx_gae_ppo_loss: 25 B/token)"}
+
+
 def reshard_c4():
     from paper_2507_13833_b200.reshard import Layout, Topology
     from paper_2507_13833_b200.store import DeviceBufferStore, StoreStagePlan
@@ -174,6 +191,7 @@ def main():
     rows = [grpo("C1", 64, 8, dfx.TokenDist("constant", 1024)),
             grpo("C2", 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096)),
             ppo_c3(),
+            ppo_c3_fused(),
             grpo("C5/8 (one GPU's share: 512 prompts)", 512, 16, dfx.TokenDist("skewed", 0, 1, 16384)),
             reshard_c4(),
             wire_c4()]
