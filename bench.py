@@ -237,10 +237,10 @@ class DagSlice:
         return [x for grp in cb.sources for x in grp if isinstance(x, RemoteSource)]
 
     def launches_per_step(self):
-        # grpo_adv + loss_slots + finalize; records crossing GPUs: + the materializing unpack kernel (lazy: none,
-        # the loss kernel reads the partner's records over NVLink)
+        # grpo_adv + slot_table + loss_slots + finalize; records crossing GPUs: + the materializing unpack kernel
+        # (lazy: none, the loss kernel reads the partner's records over NVLink; one slot table per source)
         # (TP-split: + dfx_loss_combine after the 56-byte all-gather)
-        return 3 + (1 if self.cross and (not self.lazy or self.tp_group is not None) else 0)
+        return 4 + (1 if self.cross else 0)
 
     def describe(self):
         if not self.cross:

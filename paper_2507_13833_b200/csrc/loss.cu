@@ -118,6 +118,13 @@ __device__ __forceinline__ int src_of_roll(const LossSrc* src, int n_src, int64_
   return k;
 }
 
+struct SlotEnt {
+  uint32_t toff;  // t0 - base
+  int32_t s;      // rollout (source-local)
+  int32_t len;    // tokens; 0 = empty slot id
+  float A;        // DFX_ADV_ROLLOUT: f32(adv_roll[s])
+};
+
 struct LossParams {
   int n_src;
   LossSrc src[kMaxLossSrc];
@@ -142,9 +149,39 @@ struct LossParams {
   const double* seq_n;     // dlogp: per-rollout mask count
   const double* grp_stats; // dlogp: per loss group {N, S}
   double* part;            // [5][n_slots]
+  const SlotEnt* tab;      // [n_slots] slot table (global slot ids)
   int32_t* flags;
   unsigned long long* ticket;  // [kMaxLossSrc + 1] per-source slot tickets + finished warps; zero on entry, restored
 };
+
+// ---- slot table -------------------------------------------------------------------------------------------------
+// One 16-byte entry per slot id: the slot's rollout, its token range and (per-rollout advantage) the advantage,
+// built by a thread-per-rollout pre-pass, so the streaming warps resolve a claimed slot with ONE load instead of
+// the 32-ary search over cu_seqlens (three dependent L2 round trips) plus the advantage load.
+
+// thread per rollout s: the entries of slot ids [f(s), f(s+1)) (f(s) = s + window of cu[s]; the last rollout
+// also owns the ids up to the source's slot count)
+__global__ void __launch_bounds__(256) slot_table_kernel(SlotGeom g, int64_t n_slots, const double* __restrict__ adv,
+                                                         SlotEnt* __restrict__ tab) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= g.n_seq) return;
+  const int64_t a = __ldg(g.cu + s), b = __ldg(g.cu + s + 1);
+  const int64_t f0 = s + ((a - g.base) >> g.sh);
+  const int64_t f1 = s + 1 < g.n_seq ? s + 1 + ((b - g.base) >> g.sh) : n_slots;
+  const int64_t wa = (a - g.base) >> g.sh, wb = (b - 1 - g.base) >> g.sh;
+  const float A = adv ? (float)__ldg(adv + s) : 0.0f;
+  for (int64_t u = f0; u < f1; ++u) {
+    const int64_t w = u - s;
+    SlotEnt e{0u, (int32_t)s, 0, A};
+    if (b > a && w >= wa && w <= wb) {
+      const int64_t ws = g.base + (w << g.sh);
+      const int64_t t0 = max(a, ws), t1 = min(b, ws + ((int64_t)1 << g.sh));
+      e.toff = (uint32_t)(t0 - g.base);
+      e.len = (int32_t)(t1 - t0);
+    }
+    tab[u] = e;
+  }
+}
 
 // ---- per-token math (k3_series, clip_exact_f32: common.cuh) ---------------------------------------------
 struct TokAcc {
@@ -283,6 +320,42 @@ __device__ __forceinline__ GroupStats group_stats_warp(const double* __restrict_
   return {mean, __dadd_rn(sd, eps)};
 }
 
+// Fused GRPO (DFX_ADV_GROUP_FUSED): the slot table pre-pass also computes the advantages -- warp per record: the
+// bit-exact f64 group statistics once, the rollouts' f64 advantage channel, and every slot entry of the record's
+// rollouts with its f32 advantage (the streaming kernel then needs no reward loads and no f64 chain per slot)
+__global__ void __launch_bounds__(256) slot_table_group_kernel(SlotGeom g, int64_t n_slots, int64_t n_records,
+                                                               const int32_t* __restrict__ go,
+                                                               const double* __restrict__ reward, double eps,
+                                                               double* __restrict__ adv_out, int32_t* flags,
+                                                               SlotEnt* __restrict__ tab) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_records) return;
+  const int32_t ra = go[r], rb = go[r + 1];
+  GroupStats gs{0.0, 1.0};
+  if (rb > ra) gs = group_stats_warp(reward, ra, rb, eps, lane);
+  else if (flags && lane == 0) atomicOr(flags, kFlagMissingRollouts);  // require_rollouts functions.hpp:82-87
+  for (int32_t s = ra + lane; s < rb; s += 32) {
+    const double adv = group_adv(__ldg(reward + s), gs);
+    if (adv_out) adv_out[s] = adv;
+    const int64_t a = __ldg(g.cu + s), b = __ldg(g.cu + s + 1);
+    const int64_t f0 = s + ((a - g.base) >> g.sh);
+    const int64_t f1 = s + 1 < g.n_seq ? s + 1 + ((b - g.base) >> g.sh) : n_slots;
+    const int64_t wa = (a - g.base) >> g.sh, wb = (b - 1 - g.base) >> g.sh;
+    for (int64_t u = f0; u < f1; ++u) {
+      const int64_t w = u - s;
+      SlotEnt e{0u, (int32_t)s, 0, (float)adv};
+      if (b > a && w >= wa && w <= wb) {
+        const int64_t ws = g.base + (w << g.sh);
+        const int64_t t0 = max(a, ws), t1 = min(b, ws + ((int64_t)1 << g.sh));
+        e.toff = (uint32_t)(t0 - g.base);
+        e.len = (int32_t)(t1 - t0);
+      }
+      tab[u] = e;
+    }
+  }
+}
+
 // one warp per record
 __global__ void __launch_bounds__(256) grpo_adv_kernel(int64_t n_records, const int32_t* __restrict__ go,
                                                        const double* __restrict__ reward, double eps,
@@ -330,20 +403,6 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
 
-  // Record duty (fused GRPO mode): write the f64 advantage channel of every
-  // record, including zero-length rollouts that own no slot.
-  if (ADV == DFX_ADV_GROUP_FUSED && p.adv_roll_out) {
-    for (int64_t r = gwarp; r < p.n_records; r += nwarps) {
-      const int32_t a = __ldg(p.group_off + r), b = __ldg(p.group_off + r + 1);
-      if (b <= a) {
-        if (lane == 0 && p.flags) atomicOr(p.flags, kFlagMissingRollouts);
-        continue;
-      }
-      const GroupStats gs = group_stats_warp(p.reward, a, b, p.adv_eps, lane);
-      for (int32_t s = a + lane; s < b; s += 32) p.adv_roll_out[s] = group_adv(__ldg(p.reward + s), gs);
-    }
-  }
-
   // whitening coefficients: live across the loop only for per-token advantages; the per-rollout paths whiten
   // once per slot (keeps the hot kernels' registers for loads in flight)
   double mu = 0.0, rstd = 1.0;
@@ -370,21 +429,16 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     }
     const LossSrc& S = p.src[k];
     const int64_t u = S.slot0 + ul;
-    int64_t s, t0, t1;
-    if (!slot_unit(S.g, u - S.slot0, lane, s, t0, t1)) {
+    const int4 ev = __ldg(reinterpret_cast<const int4*>(p.tab + u));  // one load resolves the slot
+    if (ev.z == 0) {
       if (lane < 5) part[(int64_t)lane * p.n_slots + u] = 0.0;
       continue;
     }
+    const int64_t s = ev.y;
+    const int64_t t0 = S.g.base + (int64_t)(uint32_t)ev.x, t1 = t0 + ev.z;
     const int64_t sg = S.roll0 + s;  // global rollout (loss groups, dlogp weights)
     float A_unit = 0.0f;
-    if (ADV == DFX_ADV_GROUP_FUSED) {
-      const int32_t grp = __ldg(p.roll_group + s);
-      const GroupStats gs = group_stats_warp(p.reward, __ldg(p.group_off + grp), __ldg(p.group_off + grp + 1),
-                                             p.adv_eps, lane);
-      A_unit = (float)group_adv(__ldg(p.reward + s), gs);
-    } else if (ADV == DFX_ADV_ROLLOUT) {
-      A_unit = (float)S.adv_roll_in[s];
-    }
+    if (ADV != DFX_ADV_TOKEN) A_unit = __int_as_float(ev.w);  // (group advantages: computed by the pre-pass)
     if (ADV != DFX_ADV_TOKEN && p.whiten) {
       double m0, r0;
       whiten_coeffs(p, m0, r0);
@@ -682,6 +736,7 @@ struct LossWs {
   double* seq_n;
   double* grp_stats;
   unsigned int* ticket;
+  SlotEnt* tab;
   int nb;
   size_t bytes;
 };
@@ -708,6 +763,7 @@ LossWs loss_ws_layout(void* base, int64_t n_seq, int64_t n_slots, int32_t n_grou
   w.blk = reinterpret_cast<double*>(take(sizeof(double) * 6 * size_t(n_groups) * size_t(w.nb)));
   w.seq_n = reinterpret_cast<double*>(take(sizeof(double) * size_t(n_seq + 1)));
   w.grp_stats = reinterpret_cast<double*>(take(sizeof(double) * 2 * size_t(n_groups)));
+  w.tab = reinterpret_cast<SlotEnt*>(take(sizeof(SlotEnt) * size_t(n_slots)));
   w.bytes = off;
   return w;
 }
@@ -890,6 +946,8 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
       default:
         return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: bad adv_source");
     }
+    if (x.token_span >= (int64_t(1) << 31))
+      return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: a source spans more than 2^31 tokens (slot table offsets)");
     if (k > 0 && (x.dlogp != nullptr) != want_dl) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: dlogp on all sources or none");
     want_dl = x.dlogp != nullptr;
     src[k].g = geom_of(b, x.token_base & ~int64_t(3), x.token_span);
@@ -970,6 +1028,20 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
   p.part = w.part;
   p.flags = args->flags;
   p.ticket = w.slot_ticket;
+  p.tab = w.tab;
+  if (cfg->adv_source == DFX_ADV_GROUP_FUSED) {  // single source: the table pre-pass computes the advantages
+    slot_table_group_kernel<<<(unsigned)((b0->n_records + 7) / 8), 256, 0, stream>>>(
+        src[0].g, n_slots, b0->n_records, b0->group_off, b0->reward, cfg->adv_eps, p.adv_roll_out, args->flags, w.tab);
+    DFX_LAUNCH_CHECK("slot_table_group_kernel");
+  }
+  for (int32_t k = 0; k < n_src && cfg->adv_source != DFX_ADV_GROUP_FUSED; ++k) {  // the slot table of every source
+    if (srcs[k].b.n_rollouts <= 0) continue;
+    const int64_t nk = (k + 1 < n_src ? src[k + 1].slot0 : n_slots) - src[k].slot0;
+    const double* adv = cfg->adv_source == DFX_ADV_ROLLOUT ? srcs[k].adv_roll : nullptr;
+    slot_table_kernel<<<(unsigned)((srcs[k].b.n_rollouts + 255) / 256), 256, 0, stream>>>(src[k].g, nk, adv,
+                                                                                        w.tab + src[k].slot0);
+    DFX_LAUNCH_CHECK("slot_table_kernel");
+  }
   if (args->ev_main_begin) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_begin), stream));
   switch (cfg->adv_source) {
     case DFX_ADV_GROUP_FUSED: launch_slots_adv<DFX_ADV_GROUP_FUSED>(p, stream, cfg->kl_type, want_dl); break;
