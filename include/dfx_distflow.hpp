@@ -10,9 +10,10 @@
 // MissingChannelError / MissingRolloutsError / IndivisibleError / LayoutError / Error, so invoke_node's wrapping
 // (worker.hpp:192-200) behaves identically.
 //
-// Packing: a SampleBatch (AoS, std::map channels) is packed into the device SoA layout (dfx_packed) per call
-// and results are written back as f64 channels -- the reference's channel type -- so the GPU advantage equals
-// fn_group_advantage bit for bit. Per-token streams for the loss come from the rollout payload when it follows
+// Packing: a SampleBatch (AoS, std::map channels) is packed into the device SoA layout (dfx_packed) through the
+// calling worker thread's arena (pinned staging + grow-only device buffers + the worker's stream: no allocation
+// in a steady state) and results are written back as f64 channels -- the reference's channel type -- so the GPU
+// advantage equals fn_group_advantage bit for bit. Per-token streams for the loss come from the rollout payload when it follows
 // the documented layout: token_id i32[L] | lp f32[L] | old_lp f32[L] | ref_lp f32[L] | mask u8[L]
 // (17 bytes per token).
 #pragma once
@@ -95,6 +96,56 @@ std::vector<T> download(const DeviceBuffer& b, size_t n) {
   return v;
 }
 
+// ---- per-worker device arena ---------------------------------------------------------------------------------
+// The reference's StageContext (functions.hpp:55-61) has no slot for device state, and one OS thread runs each
+// worker's chain (runner.hpp:525-530): the arena is thread-local -- the worker's own stream, grow-only device
+// buffers and pinned host staging, reused by every node call, so a steady-state run_iteration allocates nothing
+// and every host<->device copy is an async pinned transfer on the worker's stream (one synchronization per node).
+struct PinnedBuffer {
+  void* p = nullptr;
+  size_t n = 0;
+  PinnedBuffer() = default;
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  ~PinnedBuffer() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+struct Arena {
+  cudaStream_t stream = nullptr;
+  std::map<std::string, DeviceBuffer> dev;
+  std::map<std::string, PinnedBuffer> host;
+  uint64_t grows = 0;  // allocations so far (a steady state stops growing)
+  Arena() { cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate"); }
+  ~Arena() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+  // device buffer `name` of at least `bytes` (zero-filled when it grows: workspaces rely on it)
+  void* device(const std::string& name, size_t bytes) {
+    DeviceBuffer& d = dev[name];
+    if (d.n < bytes) {
+      d = DeviceBuffer(std::max<size_t>(bytes, 2 * d.n), true);
+      ++grows;
+    }
+    return d.p;
+  }
+  void* pinned(const std::string& name, size_t bytes) {
+    PinnedBuffer& h = host[name];
+    if (h.n < bytes) {
+      if (h.p) cudaFreeHost(h.p);
+      h.n = std::max<size_t>(bytes, 2 * h.n);
+      cuda_check(cudaMallocHost(&h.p, h.n), "cudaMallocHost");
+      ++grows;
+    }
+    return h.p;
+  }
+};
+inline Arena& worker_arena() {
+  static thread_local Arena a;
+  return a;
+}
+
 // ---- packed batch ----------------------------------------------------------------------------------------
 struct PackOptions {
   std::vector<std::string> channels;  // rollout channels to upload (f64), e.g. {"reward"}
@@ -103,84 +154,100 @@ struct PackOptions {
 
 struct DevicePacked {
   int64_t n_records = 0, n_rollouts = 0, n_tokens = 0;
-  DeviceBuffer group_off, roll_group, cu;
-  std::map<std::string, DeviceBuffer> ch;
-  DeviceBuffer lp, old_lp, ref_lp, mask;
+  std::map<std::string, double*> ch;  // device channel arrays (arena)
   dfx_packed view{};
 };
 
 constexpr uint32_t kPayloadBytesPerToken = 17;
 
-// Packs a reference SampleBatch into device SoA. Follows detail::require_rollouts / channel_of
-// (functions.hpp:82-93): a record without rollouts raises MissingRolloutsError, a rollout without a requested
-// channel raises MissingChannelError.
-inline DevicePacked pack(const distflow::SampleBatch& batch, const PackOptions& opt) {
+// Packs a reference SampleBatch into device SoA through the worker's arena: one pass over the records writes
+// the SoA arrays into pinned staging, then one async H2D copy per array on the worker's stream. Follows
+// detail::require_rollouts / channel_of (functions.hpp:82-93): a record without rollouts raises
+// MissingRolloutsError, a rollout without a requested channel raises MissingChannelError.
+inline DevicePacked pack(const distflow::SampleBatch& batch, const PackOptions& opt, Arena& ar = worker_arena()) {
   DevicePacked d;
-  std::vector<int32_t> go{0}, rg;
-  std::vector<int64_t> cu{0};
-  std::map<std::string, std::vector<double>> ch;
-  std::vector<float> lp, old_lp, ref_lp;
-  std::vector<uint8_t> mask;
-  for (size_t r = 0; r < batch.records.size(); ++r) {
-    const auto& rec = batch.records[r];
+  int64_t R = int64_t(batch.records.size()), S = 0, T = 0;
+  for (const auto& rec : batch.records) {
     distflow::detail::require_rollouts(rec);
-    for (const auto& ro : rec.rollouts) {
-      for (const auto& name : opt.channels) ch[name].push_back(distflow::detail::channel_of(ro, name));
+    S += int64_t(rec.rollouts.size());
+    if (opt.token_streams)
+      for (const auto& ro : rec.rollouts) {
+        if (ro.payload.size() != uint64_t(ro.token_count) * kPayloadBytesPerToken)
+          throw distflow::Error("payload of record " + std::to_string(rec.sample_id) +
+                                " does not follow the 17 B/token stream layout");
+        T += ro.token_count;
+      }
+  }
+  const size_t pad = 16;  // aligned over-read slack (dfx.h packed-batch contract)
+  auto* go = static_cast<int32_t*>(ar.pinned("go", size_t(R + 1) * 4));
+  auto* rg = static_cast<int32_t*>(ar.pinned("rg", size_t(S) * 4 + 4));
+  auto* cu = static_cast<int64_t*>(ar.pinned("cu", size_t(S + 1) * 8));
+  std::vector<double*> chh;
+  for (const auto& name : opt.channels) chh.push_back(static_cast<double*>(ar.pinned("ch:" + name, size_t(S) * 8 + 8)));
+  float *lp = nullptr, *old = nullptr, *ref = nullptr;
+  uint8_t* mask = nullptr;
+  if (opt.token_streams) {
+    lp = static_cast<float*>(ar.pinned("lp", size_t(T) * 4 + 4));
+    old = static_cast<float*>(ar.pinned("old", size_t(T) * 4 + 4));
+    ref = static_cast<float*>(ar.pinned("ref", size_t(T) * 4 + 4));
+    mask = static_cast<uint8_t*>(ar.pinned("mask", size_t(T) + 1));
+  }
+  go[0] = 0;
+  cu[0] = 0;
+  int64_t s = 0, t = 0;
+  for (size_t r = 0; r < batch.records.size(); ++r) {
+    for (const auto& ro : batch.records[r].rollouts) {
+      for (size_t c = 0; c < opt.channels.size(); ++c) chh[c][s] = distflow::detail::channel_of(ro, opt.channels[c]);
       int64_t L = 0;
       if (opt.token_streams) {
         L = ro.token_count;
-        if (ro.payload.size() != uint64_t(L) * kPayloadBytesPerToken)
-          throw distflow::Error("payload of record " + std::to_string(rec.sample_id) +
-                                " does not follow the 17 B/token stream layout");
         const uint8_t* p = ro.payload.data() + 4 * L;  // skip token ids
-        auto append_f32 = [&](std::vector<float>& dst, const uint8_t* src) {
-          const size_t at = dst.size();
-          dst.resize(at + size_t(L));
-          std::memcpy(dst.data() + at, src, size_t(L) * 4);
-        };
-        append_f32(lp, p);
-        append_f32(old_lp, p + 4 * L);
-        append_f32(ref_lp, p + 8 * L);
-        mask.insert(mask.end(), p + 12 * L, p + 13 * L);
+        std::memcpy(lp + t, p, size_t(L) * 4);
+        std::memcpy(old + t, p + 4 * L, size_t(L) * 4);
+        std::memcpy(ref + t, p + 8 * L, size_t(L) * 4);
+        std::memcpy(mask + t, p + 12 * L, size_t(L));
       }
-      cu.push_back(cu.back() + L);
-      rg.push_back(int32_t(r));
+      t += L;
+      cu[s + 1] = t;
+      rg[s++] = int32_t(r);
     }
-    go.push_back(int32_t(rg.size()));
+    go[r + 1] = int32_t(s);
   }
-  d.n_records = int64_t(batch.records.size());
-  d.n_rollouts = int64_t(rg.size());
-  d.n_tokens = cu.back();
-  d.group_off = upload(go);
-  d.roll_group = upload(rg);
-  d.cu = upload(cu);
-  for (auto& [name, v] : ch) d.ch.emplace(name, upload(v));
-  const size_t pad = 16;  // aligned over-read slack (dfx.h packed-batch contract)
-  if (opt.token_streams) {
-    d.lp = upload(lp, pad);
-    d.old_lp = upload(old_lp, pad);
-    d.ref_lp = upload(ref_lp, pad);
-    d.mask = upload(mask, pad);
-  }
+  auto up = [&](const char* name, const void* src, size_t bytes, size_t dev_bytes) {
+    void* dst = ar.device(name, dev_bytes);
+    if (bytes) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ar.stream), "H2D");
+    return dst;
+  };
+  d.n_records = R;
+  d.n_rollouts = S;
+  d.n_tokens = T;
   dfx_packed& v = d.view;
-  v.n_records = d.n_records;
-  v.n_rollouts = d.n_rollouts;
-  v.group_off = d.group_off.as<int32_t>();
-  v.roll_group = d.roll_group.as<int32_t>();
-  v.cu_seqlens = d.cu.as<int64_t>();
-  auto chp = [&](const char* n) { auto it = d.ch.find(n); return it == d.ch.end() ? nullptr : it->second.as<double>(); };
+  v.n_records = R;
+  v.n_rollouts = S;
+  v.group_off = static_cast<int32_t*>(up("go", go, size_t(R + 1) * 4, size_t(R + 1) * 4));
+  v.roll_group = static_cast<int32_t*>(up("rg", rg, size_t(S) * 4, size_t(S) * 4 + 4));
+  v.cu_seqlens = static_cast<int64_t*>(up("cu", cu, size_t(S + 1) * 8, size_t(S + 1) * 8));
+  for (size_t c = 0; c < opt.channels.size(); ++c)
+    d.ch[opt.channels[c]] = static_cast<double*>(up(("ch:" + opt.channels[c]).c_str(), chh[c], size_t(S) * 8, size_t(S) * 8 + 8));
+  auto chp = [&](const char* n) { auto it = d.ch.find(n); return it == d.ch.end() ? nullptr : it->second; };
   v.reward = chp("reward");
   v.value = chp("value");
-  v.lp = d.lp.as<float>();
-  v.old_lp = d.old_lp.as<float>();
-  v.ref_lp = d.ref_lp.as<float>();
-  v.mask = d.mask.as<uint8_t>();
+  if (opt.token_streams) {
+    v.lp = static_cast<float*>(up("lp", lp, size_t(T) * 4, (size_t(T) + pad) * 4));
+    v.old_lp = static_cast<float*>(up("old", old, size_t(T) * 4, (size_t(T) + pad) * 4));
+    v.ref_lp = static_cast<float*>(up("ref", ref, size_t(T) * 4, (size_t(T) + pad) * 4));
+    v.mask = static_cast<uint8_t*>(up("mask", mask, size_t(T), size_t(T) + pad));
+  }
   return d;
 }
 
-// Write a per-rollout f64 device array back as channel `name` (std::map insert, like the reference).
-inline void write_channel(distflow::SampleBatch& batch, const std::string& name, const DeviceBuffer& dev, int64_t n) {
-  const auto host = download<double>(dev, size_t(n));
+// Write a per-rollout f64 device array back as channel `name` (std::map insert, like the reference): one async
+// D2H into pinned staging, one synchronization of the worker's stream.
+inline void write_channel(distflow::SampleBatch& batch, const std::string& name, const double* dev, int64_t n,
+                          Arena& ar = worker_arena()) {
+  auto* host = static_cast<double*>(ar.pinned("out:" + name, size_t(n) * 8 + 8));
+  if (n) cuda_check(cudaMemcpyAsync(host, dev, size_t(n) * 8, cudaMemcpyDeviceToHost, ar.stream), "D2H");
+  cuda_check(cudaStreamSynchronize(ar.stream), "sync");
   size_t s = 0;
   for (auto& rec : batch.records)
     for (auto& ro : rec.rollouts) ro.channels[name] = host[s++];
@@ -207,12 +274,14 @@ inline dfx_loss_out& last_loss() {
 inline void gpu_group_advantage(const distflow::NodeSpec& node, distflow::SampleBatch& batch,
                                 distflow::StageContext& ctx) {
   (void)node;
-  DevicePacked d = pack(batch, PackOptions{{"reward"}, false});
-  DeviceBuffer adv(sizeof(double) * size_t(d.n_rollouts));
-  DeviceBuffer flags(sizeof(int32_t), true);
-  check(dfx_grpo_advantage(&d.view, ctx.advantage_eps, adv.as<double>(), flags.as<int32_t>(), nullptr));
-  check(dfx_check_flags(flags.as<int32_t>(), nullptr));
-  write_channel(batch, "advantage", adv, d.n_rollouts);
+  Arena& ar = worker_arena();
+  DevicePacked d = pack(batch, PackOptions{{"reward"}, false}, ar);
+  auto* adv = static_cast<double*>(ar.device("adv", sizeof(double) * size_t(d.n_rollouts) + 8));
+  auto* flags = static_cast<int32_t*>(ar.device("flags", sizeof(int32_t)));
+  cuda_check(cudaMemsetAsync(flags, 0, sizeof(int32_t), ar.stream), "memset");
+  check(dfx_grpo_advantage(&d.view, ctx.advantage_eps, adv, flags, ar.stream));
+  check(dfx_check_flags(flags, ar.stream));
+  write_channel(batch, "advantage", adv, d.n_rollouts, ar);
 }
 
 // fn_ppo_advantage (functions.hpp:163-172): advantage = reward - value.
@@ -220,11 +289,11 @@ inline void gpu_ppo_advantage(const distflow::NodeSpec& node, distflow::SampleBa
                               distflow::StageContext& ctx) {
   (void)node;
   (void)ctx;
-  DevicePacked d = pack(batch, PackOptions{{"reward", "value"}, false});
-  DeviceBuffer adv(sizeof(double) * size_t(d.n_rollouts));
-  check(dfx_ppo_advantage(&d.view, adv.as<double>(), nullptr));
-  cuda_check(cudaDeviceSynchronize(), "sync");
-  write_channel(batch, "advantage", adv, d.n_rollouts);
+  Arena& ar = worker_arena();
+  DevicePacked d = pack(batch, PackOptions{{"reward", "value"}, false}, ar);
+  auto* adv = static_cast<double*>(ar.device("adv", sizeof(double) * size_t(d.n_rollouts) + 8));
+  check(dfx_ppo_advantage(&d.view, adv, ar.stream));
+  write_channel(batch, "advantage", adv, d.n_rollouts, ar);
 }
 
 // fn_train (functions.hpp:176-182) with the loss on the GPU: when the rollouts carry the token-stream payload and
@@ -239,18 +308,22 @@ inline void gpu_train(const distflow::NodeSpec& node, distflow::SampleBatch& bat
       if (ro.payload.size() != uint64_t(ro.token_count) * kPayloadBytesPerToken || !ro.channels.count("advantage"))
         streams = false;
   if (streams) {
-    DevicePacked d = pack(batch, PackOptions{{"advantage"}, true});
+    Arena& ar = worker_arena();
+    DevicePacked d = pack(batch, PackOptions{{"advantage"}, true}, ar);
     const LossConfig& lc = loss_config();
     dfx_loss_cfg cfg{lc.clip_low, lc.clip_high, lc.beta, ctx.advantage_eps, lc.kl_type, lc.agg, DFX_ADV_ROLLOUT, 0};
-    DeviceBuffer out(sizeof(dfx_loss_out));
+    auto* out = static_cast<dfx_loss_out*>(ar.device("loss_out", sizeof(dfx_loss_out)));
     dfx_loss_args a{};
-    a.adv_roll = d.ch.at("advantage").as<double>();
+    a.adv_roll = d.ch.at("advantage");
     a.n_loss_groups = 1;
-    a.out = out.as<dfx_loss_out>();
+    a.out = out;
     const size_t ws = dfx_ppo_loss_workspace_bytes(d.n_rollouts, d.n_tokens, 1);
-    DeviceBuffer work(ws, true);
-    check(dfx_ppo_loss(&d.view, 0, d.n_tokens, &cfg, &a, work.p, ws, nullptr));
-    last_loss() = download<dfx_loss_out>(out, 1)[0];
+    void* work = ar.device("loss_ws", ws);  // zero-filled when it grows; the kernels keep their tickets zeroed
+    check(dfx_ppo_loss(&d.view, 0, d.n_tokens, &cfg, &a, work, ws, ar.stream));
+    auto* host = static_cast<dfx_loss_out*>(ar.pinned("loss_out", sizeof(dfx_loss_out)));
+    cuda_check(cudaMemcpyAsync(host, out, sizeof(dfx_loss_out), cudaMemcpyDeviceToHost, ar.stream), "D2H");
+    cuda_check(cudaStreamSynchronize(ar.stream), "sync");
+    last_loss() = *host;
   }
   if (ctx.model_versions) ++(*ctx.model_versions)[node.role];
 }
