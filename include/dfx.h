@@ -404,6 +404,14 @@ int32_t dfx_comm_size(const dfx_comm* comm);
  * all-reduce on the stream + a D2H read; synchronizes the stream). */
 dfx_status dfx_comm_allreduce_i64(dfx_comm* comm, const int64_t* in, int64_t* out, int64_t n, dfx_stream stream);
 
+/* All-to-all of device byte buffers: this rank sends send_bytes[p] bytes at
+ * send + send_off[p] to every rank p and receives recv_bytes[p] bytes into
+ * recv + recv_off[p] (sizes agreed beforehand, e.g. through
+ * dfx_comm_allreduce_i64). One grouped NCCL call on the stream; the self part
+ * is a device copy. The transport under dfx_distflow::NcclFabric. */
+dfx_status dfx_comm_alltoallv(dfx_comm* comm, const void* send, const uint64_t* send_off, const uint64_t* send_bytes,
+                              void* recv, const uint64_t* recv_off, const uint64_t* recv_bytes, dfx_stream stream);
+
 /* A device batch in a store's schema (generic form of dfx_packed): streams and
  * channels in the schema's order; group_off is relative (group_off[0] == 0);
  * cu_seqlens are absolute token indices into the streams (st[k] points at token

@@ -1318,6 +1318,31 @@ dfx_status dfx_comm_allreduce_i64(dfx_comm* c, const int64_t* in, int64_t* out, 
   return DFX_OK;
 }
 
+dfx_status dfx_comm_alltoallv(dfx_comm* c, const void* send, const uint64_t* send_off, const uint64_t* send_bytes,
+                              void* recv, const uint64_t* recv_off, const uint64_t* recv_bytes, dfx_stream stream) {
+  if (!c || !send_off || !send_bytes || !recv_off || !recv_bytes)
+    return fail(DFX_INVALID_ARGUMENT, "dfx_comm_alltoallv: null argument");
+  const int me = c->rank;
+  if (send_bytes[me]) {  // to self: a device copy
+    if (send_bytes[me] != recv_bytes[me]) return fail(DFX_INVALID_ARGUMENT, "dfx_comm_alltoallv: self sizes differ");
+    DFX_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + recv_off[me], static_cast<const uint8_t*>(send) + send_off[me],
+                             send_bytes[me], cudaMemcpyDeviceToDevice, stream));
+  }
+  bool any = false;
+  for (int p = 0; p < c->n; ++p) any = any || (p != me && (send_bytes[p] || recv_bytes[p]));
+  if (!any) return DFX_OK;
+  DFX_NCCL(GroupStart());
+  for (int p = 0; p < c->n; ++p) {
+    if (p == me) continue;
+    if (send_bytes[p])
+      DFX_NCCL(Send(static_cast<const uint8_t*>(send) + send_off[p], send_bytes[p], ncclUint8, p, c->nccl, stream));
+    if (recv_bytes[p])
+      DFX_NCCL(Recv(static_cast<uint8_t*>(recv) + recv_off[p], recv_bytes[p], ncclUint8, p, c->nccl, stream));
+  }
+  DFX_NCCL(GroupEnd());
+  return DFX_OK;
+}
+
 dfx_status dfx_dstore_create(const dfx_dstore_cfg* cfg, dfx_comm* comm, dfx_stream stream, dfx_dstore** out) {
   if (!cfg || !comm || !out || !cfg->rank_of_worker) return fail(DFX_INVALID_ARGUMENT, "dfx_dstore_create: null argument");
   if (cfg->num_nodes == 0 || cfg->workers_per_node == 0)

@@ -21,3 +21,39 @@ def test_cpp_stage_shims_in_reference_runtime():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASSED" in r.stdout
     assert r.stdout.count("PASS ") >= 19  # incl. the C++ DeviceBufferStore vs the reference BufferStore
+
+
+@pytest.mark.gpu
+def test_cpp_nccl_fabric_fork_per_node():
+    """cpp/_build/test_fabric: the NCCL-backed Fabric (include/dfx_fabric.hpp) in the reference's fork-per-node
+    mode reproduces the InprocFabric run byte for byte (captures) and in cross-node traffic (2 GPUs)."""
+    import torch
+    binary = os.path.join(ROOT, "cpp", "_build", "test_fabric")
+    if not os.path.exists(binary):
+        pytest.skip("cpp/_build/test_fabric not built (needs the reference headers at build time)")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    r = subprocess.run(["timeout", "300", binary], capture_output=True, text=True, timeout=360)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS ") == 4, r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_dstore_host_fork_per_gpu():
+    """cpp/_build/bench_dstore: the distributed DataBuffer's C++ host (include/dfx_dstore.hpp), one forked process
+    per GPU, runs the C4 round trip (both transports) to completion."""
+    import json
+
+    import torch
+    binary = os.path.join(ROOT, "cpp", "_build", "bench_dstore")
+    if not os.path.exists(binary):
+        pytest.skip("cpp/_build/bench_dstore not built")
+    n = min(2, torch.cuda.device_count())
+    for tr in ("pull", "nccl"):
+        r = subprocess.run(["timeout", "200", binary, str(n), "5", "2", tr], capture_output=True, text=True,
+                           timeout=260)
+        assert r.returncode == 0, r.stdout + r.stderr
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["n_gpus"] == n and line["ms_per_round_trip"] > 0
+        print(line)
