@@ -13,7 +13,7 @@
 #include "common.cuh"
 
 #ifndef DFX_CLIP_MODE
-#define DFX_CLIP_MODE 0
+#define DFX_CLIP_MODE 1
 #endif
 #ifndef DFX_TOKEN_MINB
 #define DFX_TOKEN_MINB 2
@@ -141,6 +141,7 @@ struct LossParams {
   // <=> d < log(1-eps_lo), each as a float pair T32 + Tlo (clip_twosum)
   float t_hi32, t_lo32;
   float t_hi32_lo, t_lo32_lo;  // T64 - T32 (the thresholds as float pairs)
+  float clip_margin;           // (DFX_CLIP_MODE 1) |s*d - s*T32| below which the f32 decision may be wrong
   double adv_eps;
   int kl_type;
   int agg;
@@ -184,8 +185,11 @@ __global__ void __launch_bounds__(256) slot_table_kernel(SlotGeom g, int64_t n_s
 }
 
 // ---- per-token math (k3_series, clip_exact_f32: common.cuh) ---------------------------------------------
+// per lane and round: f32 sums of the surrogate / KL / log ratio; exact integer counts of clipped and masked tokens
+// (bit counts per vector instead of a multiply-add per token)
 struct TokAcc {
-  float pg, kl, akl, clip, n;
+  float pg, kl, akl;
+  uint32_t clip, n;
 };
 
 // Per-unit constants for a warp-uniform advantage A (GRPO broadcast): with
@@ -253,15 +257,30 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
   bool cl[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) dd[k] = f4_get(lv, k) - f4_get(ov, k);  // log ratio
-  // DFX_CLIP_MODE (kernel-variant sweeps only): 0 the exact decision below (default); 2 the f32 log-ratio
+  // DFX_CLIP_MODE (kernel-variant sweeps only): 1 (default) the f32 log-ratio decision, redone exactly by TwoSum
+  // for a vector holding a token within rounding distance of the threshold; 0 TwoSum for every token; 2 the f32
   // decision alone (can differ from the reference for tokens within an f32 ulp of the threshold); 3 the ratio
-  // decision s*rho > s*bound of round 1 (within a few f32 ulps). Measured at C2: 2 is ~2.5% faster than 0.
-  if constexpr (ADV != DFX_ADV_TOKEN && DFX_CLIP_MODE != 3) {
+  // decision s*rho > s*bound of round 1. Measured at C2 (bench path): 1 0.1050 ms, 0 0.1055, 2 0.1024.
+  if constexpr (ADV != DFX_ADV_TOKEN && DFX_CLIP_MODE == 1) {
+    // f32 decision, redone exactly (TwoSum) for the vector only when a token lies within rounding distance
+    bool near = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sd = ua.s * dd[k];
+      cl[k] = sd > ua.sT32;
+      near |= fabsf(sd - ua.sT32) <= p.clip_margin;
+    }
+    if (near) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cl[k] = clip_twosum(p, ua.s, ua.sT32, f4_get(lv, k), f4_get(ov, k), dd[k]);
+    }
+  } else if constexpr (ADV != DFX_ADV_TOKEN && DFX_CLIP_MODE != 3) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       cl[k] = DFX_CLIP_MODE == 2 ? ua.s * dd[k] > ua.sT32
                                  : clip_twosum(p, ua.s, ua.sT32, f4_get(lv, k), f4_get(ov, k), dd[k]);
   }
+  uint32_t onb = 0u, clb = 0u;  // this vector's masked-in and clipped tokens, as bits
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     bool on = ((mk >> (8 * k)) & 0xffu) != 0u;
@@ -284,15 +303,16 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
       pg = ua.nA * fminf(sr, ua.sb);
       if constexpr (DFX_CLIP_MODE == 3) cl[k] = sr > ua.sb;
     }
-    const float clipf = cl[k] ? 1.0f : 0.0f;
     acc.pg = fmaf(m, pg, acc.pg);
     acc.kl = fmaf(m, kl[k], acc.kl);
     acc.akl = fmaf(-m, d, acc.akl);
-    acc.clip = fmaf(m, clipf, acc.clip);
-    acc.n += m;
+    onb |= (on ? 1u : 0u) << k;
+    clb |= (cl[k] ? 1u : 0u) << k;
     aout[k] = on ? A : 0.0f;
-    if (DLOGP) gout[k] = m * w * ((clipf != 0.0f ? 0.0f : -A * rho) + p.beta * dkl[k]);
+    if (DLOGP) gout[k] = m * w * ((cl[k] ? 0.0f : -A * rho) + p.beta * dkl[k]);
   }
+  acc.n += __popc(onb);
+  acc.clip += __popc(onb & clb);
 }
 
 // Group stats with all lanes participating: lanes load the rewards in
@@ -457,7 +477,8 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
       else w = Sq > 0 ? (float)(1.0 / Sq) : 0.0f;
     }
 
-    double dpg = 0.0, dkl = 0.0, dakl = 0.0, dclip = 0.0, dn = 0.0;
+    double dpg = 0.0, dkl = 0.0, dakl = 0.0;
+    uint32_t nclip = 0u, nmask = 0u;
     const int64_t vbeg = t0 >> 2;
     const int32_t nvec = (int32_t)(((t1 + 3) >> 2) - vbeg);
     const float* lp0 = S.lp + 4 * vbeg;
@@ -482,7 +503,7 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
           if (ADV == DFX_ADV_TOKEN) av[j] = ldg_stream_f4(ad0 + 4 * i);
         }
       }
-      TokAcc acc{0.f, 0.f, 0.f, 0.f, 0.f};
+      TokAcc acc{0.f, 0.f, 0.f, 0u, 0u};
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j) {
         const int32_t i = ib + 32 * j;
@@ -504,14 +525,14 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
       dpg += acc.pg;
       dkl += acc.kl;
       dakl += acc.akl;
-      dclip += acc.clip;
-      dn += acc.n;
+      nclip += acc.clip;
+      nmask += acc.n;
     }
     dpg = warp_sum(dpg);
     dkl = warp_sum(dkl);
-    dclip = warp_sum(dclip);
+    const double dclip = (double)warp_sum(nclip);
     dakl = warp_sum(dakl);
-    dn = warp_sum(dn);
+    const double dn = (double)warp_sum(nmask);
     if (lane == 0) {
       part[u] = dpg;
       part[p.n_slots + u] = dkl;
@@ -1016,6 +1037,8 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
     p.t_lo32 = (float)t_lo;
     p.t_hi32_lo = (float)(t_hi - (double)p.t_hi32);
     p.t_lo32_lo = std::isfinite(t_lo) ? (float)(t_lo - (double)p.t_lo32) : 0.0f;
+    // f32(l - o) is within 2^-24 |l - o| of l - o, T32 within 2^-24 |T| of T; near the threshold |d| ~ |T|
+    p.clip_margin = (float)(1e-6 * (1.0 + std::max(std::fabs(t_hi), std::isfinite(t_lo) ? std::fabs(t_lo) : 0.0)));
   }
   p.beta = (float)cfg->beta;
   p.adv_eps = cfg->adv_eps;
