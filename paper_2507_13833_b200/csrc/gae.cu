@@ -9,25 +9,27 @@
 // ONE reverse scan over the whole token line, no per-rollout segmentation.
 //
 // Three launches, all stream-ordered (graph-capturable):
-//   gae_prep_kernel    thread per rollout: sets the rollout-end bit of its last token in a token bitmap and
-//                      advances the look-back epoch (safe here: the previous scan has completed); it releases the
-//                      scan as a programmatic dependent launch, so the scan's loads overlap it;
-//   gae_smem_kernel    single-pass decoupled look-back scan. One CTA per 4096-token tile, NOT persistent: block b
-//                      scans tile n_tiles-1-b, so the tiles it looks back at belong to lower block indices, which
-//                      are dispatched first (the forward-progress argument of CUB's single-pass scan). The tile is
-//                      bulk-loaded (TMA) into shared memory; each thread owns 32 tokens; every input (r, V, mask,
-//                      end bits, the token after the tile) is read without any dependent global load before the
-//                      look-back, and each thread clears the end-bit word it consumed, leaving the bitmap zero;
-//   gae_finish_kernel  (whitening only) reduces the per-tile masked sums in tile order: deterministic.
+//   gae_prep_kernel    thread per rollout: sets the rollout-end bit of its last token in a token bitmap, writes
+//                      the segment bounds (below) and advances the publish epoch (safe here: the previous scan has
+//                      completed); it releases the scan as a programmatic dependent launch;
+//   the scan           dfx_gae: gae_seg_kernel (rollout-aligned segments, persistent, TMA ring, no look-back for
+//                      rollouts up to 64K tokens); the fused dfx_gae_ppo_loss: gae_smem_kernel (one 4096-token
+//                      tile per CTA, single-pass decoupled look-back; block b scans tile n_tiles-1-b, so the tiles it
+//                      looks back at belong to lower block indices, dispatched first -- the forward-progress
+//                      argument of CUB's single-pass scan). Both stage their tiles with bulk copies (TMA) and every
+//                      reader clears the end bits it consumed, leaving the bitmap zero between calls;
+//   gae_finish_kernel  (whitening only) reduces the per-segment / per-tile masked sums in order: deterministic.
 // Tile state is one 16-byte record per tile {f64 x ; f32 c ; u32 tag} written and polled with single relaxed
 // 128-bit accesses, so value and status are never seen out of order and no fence is needed (on sm_100 a gpu-scope
 // fence or acquire invalidates L1: CCTL.IVALL, measured as the top stall of a fenced version).
 // Arithmetic: f32 inputs and outputs; deltas, chunk maps, scans and the per-token recurrence in f64. HBM-bound:
-// 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map. Design history: profiles/r01_gae_experiments.md.
+// 17 B/token (r, V, mask in; A, R out) + 1 bit/token end map. Design history: profiles/r01_gae_experiments.md,
+// profiles/r02_gae_segments.md.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -62,7 +64,17 @@ struct GaeParams {
   int kl_type;
   double* lpart;                  // [5][n_tiles] per-tile loss sums {pg, kl, approx_kl, clip, n}
   uint8_t* seq_has;               // [n_seq] rollout has a masked token (prep), summed in order by the finish
+  // rollout-aligned segments (gae_seg_kernel)
+  int64_t seg_len;                // nominal segment length S
+  int64_t n_segs;
+  unsigned long long* seg_start;  // [n_segs + 1] segment starts (bit 62: the start cuts a rollout)
+  unsigned long long* trace;      // (DFX_GAE_TRACE, diagnostics only) per-CTA globaltimer stamps
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Aff {
   double d, c;  // X -> d + c X
@@ -85,43 +97,51 @@ __device__ __forceinline__ double rec_x(const ulonglong2& r) { return __longlong
 __device__ __forceinline__ double rec_c(const ulonglong2& r) { return (double)__uint_as_float((unsigned int)r.y); }
 
 // ---- prep: rollout-end bitmap + epoch ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) gae_prep_kernel(const int64_t* __restrict__ cu, int64_t n_seq, int64_t base,
-                                                       uint32_t* __restrict__ ends, unsigned long long* ticket) {
-  // the scan kernel is launched as a programmatic dependent: let it start its loads now; it waits for this
-  // grid's completion (griddepcontrol.wait) before reading the bitmap or the epoch
+__device__ __forceinline__ void seg_bounds_from_start(const GaeParams& p, int64_t s);
+
+__global__ void __launch_bounds__(256) gae_prep_kernel(GaeParams p) {
+  // the scan kernel is launched as a programmatic dependent: let it start now; it waits for this grid's
+  // completion (griddepcontrol.wait) before reading the bitmap, the segment bounds or the epoch
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == 0) ticket[2] = (ticket[2] + 1ull) & 0x3fffffffull;
-  if (s >= n_seq) return;
-  const int64_t a = __ldg(cu + s), b = __ldg(cu + s + 1);
+  if (s == 0) {
+    p.ticket[2] = (p.ticket[2] + 1ull) & 0x3fffffffull;
+    p.ticket[0] = 0ull;  // segment claims
+  }
+  if (s > p.n_seq) return;
+  if (p.seg_start) seg_bounds_from_start(p, s);
+  if (s == p.n_seq) return;
+  const int64_t a = __ldg(p.cu + s), b = __ldg(p.cu + s + 1);
   if (b <= a) return;  // empty rollouts own no token
-  const int64_t e = b - 1 - base;
-  atomicOr(ends + (e >> 5), 1u << (e & 31));
+  const int64_t e = b - 1 - p.base;
+  atomicOr(reinterpret_cast<uint32_t*>(p.ends) + (e >> 5), 1u << (e & 31));
 }
 
-// fused variant: warp per rollout -- the end bit, the look-back epoch, and whether the rollout has a masked token
-// (the sequence count of the loss), found with 16-byte mask loads and an early exit
-__global__ void __launch_bounds__(256) gae_prep_loss_kernel(const int64_t* __restrict__ cu, int64_t n_seq,
-                                                            int64_t base, uint32_t* __restrict__ ends,
-                                                            unsigned long long* ticket,
-                                                            const uint8_t* __restrict__ mask, uint8_t* seq_has) {
+// fused variant: warp per rollout -- the end bit, the segment bounds, the epoch, and whether the rollout has a
+// masked token (the sequence count of the loss), found with 16-byte mask loads and an early exit
+__global__ void __launch_bounds__(256) gae_prep_loss_kernel(GaeParams p) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (s == 0 && lane == 0) ticket[2] = (ticket[2] + 1ull) & 0x3fffffffull;
-  if (s >= n_seq) return;
-  const int64_t a = __ldg(cu + s), b = __ldg(cu + s + 1);
+  if (s == 0 && lane == 0) {
+    p.ticket[2] = (p.ticket[2] + 1ull) & 0x3fffffffull;
+    p.ticket[0] = 0ull;
+  }
+  if (s > p.n_seq) return;
+  if (lane == 0 && p.seg_start) seg_bounds_from_start(p, s);
+  if (s == p.n_seq) return;
+  const int64_t a = __ldg(p.cu + s), b = __ldg(p.cu + s + 1);
   bool has = false;
   if (b > a) {
     if (lane == 0) {
-      const int64_t e = b - 1 - base;
-      atomicOr(ends + (e >> 5), 1u << (e & 31));
+      const int64_t e = b - 1 - p.base;
+      atomicOr(reinterpret_cast<uint32_t*>(p.ends) + (e >> 5), 1u << (e & 31));
     }
     for (int64_t t0 = a & ~int64_t(15); t0 < b && !has; t0 += 512) {
       const int64_t t = t0 + 16 * lane;
       uint32_t any = 0;
       if (t < b) {
-        const uint4 v = *reinterpret_cast<const uint4*>(mask + t);
+        const uint4 v = *reinterpret_cast<const uint4*>(p.mask + t);
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -132,7 +152,7 @@ __global__ void __launch_bounds__(256) gae_prep_loss_kernel(const int64_t* __res
       has = __any_sync(kFull, any);
     }
   }
-  if (lane == 0) seq_has[s] = has ? 1 : 0;
+  if (lane == 0) p.seq_has[s] = has ? 1 : 0;
 }
 
 // ---- the scan ---------------------------------------------------------------------------------------------------
@@ -197,15 +217,66 @@ template <int THREADS>
 struct SmemTile {
   static constexpr int TILE = THREADS * 32;
   static constexpr uint32_t kR = 0, kV = TILE * 4 + 16, kM = 2 * (TILE * 4 + 16), kBytes = kM + TILE + 16;
-  // fused loss: lp, old, ref of the tile after the mask
-  static constexpr uint32_t kL = (kBytes + 127) & ~127u, kO = kL + TILE * 4, kF = kO + TILE * 4,
-                            kBytesLoss = kF + TILE * 4;
 };
 
-#ifndef DFX_GAE_LOSS_SMEM
-#define DFX_GAE_LOSS_SMEM 0  // fused loss inputs: 0 = L2 prefetch + per-thread loads, 1 = TMA into shared memory
-#endif
-constexpr bool kLossSmem = DFX_GAE_LOSS_SMEM != 0;
+
+// Fused loss terms of one tile after pass 2 (oracle dfo_ppo_loss per masked token), read coalesced: thread tid
+// takes the 4-token vectors tid, tid + THREADS, ... -- A and the mask from shared memory (pass 2 wrote A over r),
+// lp / old / ref from L2 (prefetched when the tile's loads were issued). Tokens outside [rb, re) are another
+// tile's or segment's. Exact integer counts of clipped and masked tokens.
+template <int THREADS>
+__device__ __forceinline__ void gae_tile_loss(const GaeParams& p, int64_t T0, uint32_t n, int64_t rb, int64_t re,
+                                              const float* s_a, const uint8_t* s_m, float& lpg, float& lkl,
+                                              float& lakl, uint32_t& lclip, uint32_t& lcnt) {
+  constexpr int kU = 4;  // vectors in flight per thread
+  const int32_t lo = (int32_t)max((int64_t)-1, min((int64_t)n, rb - T0));
+  const int32_t hi = (int32_t)max((int64_t)0, min((int64_t)n, re - T0));
+  for (uint32_t i0 = 4u * threadIdx.x; i0 < n; i0 += 4u * THREADS * kU) {
+    float4 l4[kU], o4[kU], f4[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + 4u * THREADS * u;
+      if (i < n) {
+        l4[u] = __ldcg(reinterpret_cast<const float4*>(p.lp + T0 + i));
+        o4[u] = __ldcg(reinterpret_cast<const float4*>(p.old_lp + T0 + i));
+        f4[u] = __ldcg(reinterpret_cast<const float4*>(p.ref_lp + T0 + i));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + 4u * THREADS * u;
+      if (i >= n) break;
+      const float4 a4 = *reinterpret_cast<const float4*>(s_a + i);
+      const uint32_t m4 = *reinterpret_cast<const uint32_t*>(s_m + i);
+      uint32_t onb = 0u, clb = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // (branch-free: masked-out tokens contribute zero)
+        const int32_t ti = (int32_t)i + k;
+        const bool on = ((m4 >> (8 * k)) & 0xffu) && ti >= lo && ti < hi;
+        const float m = on ? 1.0f : 0.0f;
+        const float l = f4_get(l4[u], k), o = f4_get(o4[u], k), rf = f4_get(f4[u], k), A = f4_get(a4, k);
+        const float d = l - o;
+        const float rho = exp2f(d * kLog2e);
+        const float rc = fminf(fmaxf(rho, p.lo1), p.hi1);
+        lpg = fmaf(m, fmaxf(-A * rho, -A * rc), lpg);
+        const float sg = A < 0.0f ? -1.0f : 1.0f;
+        const float sT = A > 0.0f ? p.t_hi32 : (A < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
+        const bool cl = clip_exact_f32(sg, sT, sg > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo, l, o, d);
+        const float x = rf - l;
+        float kl = 0.0f;
+        if (p.kl_type == DFX_KL_K3) kl = fabsf(x) < kK3Series ? k3_series(x) : fminf(fmaxf(expm1f(x) - x, -10.0f), 10.0f);
+        else if (p.kl_type == DFX_KL_K1) kl = -x;
+        else if (p.kl_type == DFX_KL_K2) kl = 0.5f * x * x;
+        lkl = fmaf(m, kl, lkl);
+        lakl = fmaf(-m, d, lakl);
+        onb |= (on ? 1u : 0u) << k;
+        clb |= (cl ? 1u : 0u) << k;
+      }
+      lcnt += __popc(onb);
+      lclip += __popc(onb & clb);
+    }
+  }
+}
 
 template <int THREADS, int MINB, bool WHITEN, bool LOSS = false>
 __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
@@ -219,9 +290,6 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   __shared__ Aff s_warp[NW];
   __shared__ double s_X;
   __shared__ double s_red[NW][LOSS ? 5 : 3];
-  const float* s_l = reinterpret_cast<const float*>(sm + L::kL);
-  const float* s_o = reinterpret_cast<const float*>(sm + L::kO);
-  const float* s_f = reinterpret_cast<const float*>(sm + L::kF);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t tile = p.n_tiles - 1 - (int64_t)blockIdx.x;
   const int64_t T0 = p.base + tile * TILE;
@@ -233,15 +301,11 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     mbar_fence_init();
-    mbar_arrive_expect_tx(&s_bar, (LOSS && kLossSmem ? 21u : 9u) * n);
+    mbar_arrive_expect_tx(&s_bar, 9u * n);
     tma_load_1d(s_r, p.rew + T0, 4u * n, &s_bar);
     tma_load_1d(s_v, p.val + T0, 4u * n, &s_bar);
     tma_load_1d(s_m, p.mask + T0, n, &s_bar);
-    if (LOSS && kLossSmem) {
-      tma_load_1d(sm + L::kL, p.lp + T0, 4u * n, &s_bar);
-      tma_load_1d(sm + L::kO, p.old_lp + T0, 4u * n, &s_bar);
-      tma_load_1d(sm + L::kF, p.ref_lp + T0, 4u * n, &s_bar);
-    } else if (LOSS) {  // into L2 now, read per thread in pass 2 (keeps shared memory -- and occupancy -- as GAE's)
+    if (LOSS) {  // into L2 now, read per thread in pass 2 (keeps shared memory -- and occupancy -- as GAE's)
       l2_prefetch(p.lp + T0, 4u * n);
       l2_prefetch(p.old_lp + T0, 4u * n);
       l2_prefetch(p.ref_lp + T0, 4u * n);
@@ -356,7 +420,6 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   const double Xin = fma(E.c, Xd, E.d);
   double X = fma(Tc, Xin, Td);
   float wa = 0.0f, wa2 = 0.0f;
-  float lpg = 0.0f, lkl = 0.0f, lakl = 0.0f, lclip = 0.0f;  // fused loss sums over this thread's tokens
   float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
   int pend_i = -1;
 #pragma unroll
@@ -369,13 +432,6 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
     if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
     const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
-    float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), o4 = l4, f4 = l4;
-    if (LOSS && !kLossSmem && T0 + tid * 32 + ch * 4 + 4 <= rd_end) {  // (L2 hits: prefetched at the start)
-      const int64_t g = T0 + tid * 32 + ch * 4;
-      l4 = *reinterpret_cast<const float4*>(p.lp + g);
-      o4 = *reinterpret_cast<const float4*>(p.old_lp + g);
-      f4 = *reinterpret_cast<const float4*>(p.ref_lp + g);
-    }
     float oa[4], orr[4];
 #pragma unroll
     for (int k = 3; k >= 0; --k) {
@@ -392,28 +448,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
         wa = fmaf(mw, oa[k], wa);
         wa2 = fmaf(mw * oa[k], oa[k], wa2);
       }
-      if (LOSS && (((mbits & ~ident) >> q) & 1u)) {  // the PPO terms of a masked token (oracle dfo_ppo_loss)
-        const int i = i0 + k;
-        const float l = kLossSmem ? s_l[i] : f4_get(l4, k), o = kLossSmem ? s_o[i] : f4_get(o4, k),
-                    rf = kLossSmem ? s_f[i] : f4_get(f4, k), A = oa[k];
-        const float d = l - o;
-        const float rho = exp2f(d * kLog2e);
-        const float rc = fminf(fmaxf(rho, p.lo1), p.hi1);
-        lpg += fmaxf(-A * rho, -A * rc);
-        const float sg = A < 0.0f ? -1.0f : 1.0f;
-        const float sT = A > 0.0f ? p.t_hi32 : (A < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
-        lclip += clip_exact_f32(sg, sT, sg > 0.0f ? p.t_hi32_lo : -p.t_lo32_lo, l, o, d) ? 1.0f : 0.0f;
-        const float x = rf - l;
-        float kl = 0.0f;
-        if (p.kl_type == DFX_KL_K3) kl = fabsf(x) < kK3Series ? k3_series(x) : fminf(fmaxf(expm1f(x) - x, -10.0f), 10.0f);
-        else if (p.kl_type == DFX_KL_K1) kl = -x;
-        else if (p.kl_type == DFX_KL_K2) kl = 0.5f * x * x;
-        lkl += kl;
-        lakl -= d;
-      }
     }
+    if (interior || LOSS) *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
     if (interior) {
-      *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
       pendR = make_float4(orr[0], orr[1], orr[2], orr[3]);
       pend_i = i0;
     } else {
@@ -427,18 +464,21 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     }
   }
   if (interior) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
-  if (interior) {
+  if (interior || LOSS) {
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (interior && tid == 0) {
       if (!LOSS || p.adv) tma_store_1d(p.adv + T0, s_r, 4u * TILE);  // (fused: the advantage stays on chip)
       tma_store_1d(p.ret + T0, s_v, 4u * TILE);
       tma_store_commit_and_wait();
     }
   }
   if (LOSS) {  // per-tile loss sums: fixed-shape block reduction, summed over tiles in order by the finish kernel
+    float lpg = 0.0f, lkl = 0.0f, lakl = 0.0f;
+    uint32_t lclip = 0u, lcnt = 0u;
+    gae_tile_loss<THREADS>(p, T0, n, p.begin, p.end, s_r, s_m, lpg, lkl, lakl, lclip, lcnt);
     const double v5[5] = {warp_sum((double)lpg), warp_sum((double)lkl), warp_sum((double)lakl),
-                          warp_sum((double)lclip), warp_sum((double)__popc(mbits & ~ident))};
+                          (double)warp_sum(lclip), (double)warp_sum(lcnt)};
     if (lane == 0)
       for (int q = 0; q < 5; ++q) s_red[wid][q] = v5[q];
     __syncthreads();
@@ -465,6 +505,363 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
       p.part[(int64_t)tid * p.n_tiles + tile] = t3;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// Rollout-aligned segments (default). The token line is cut into segments of about S tokens whose boundaries are
+// rollout starts: segment j = [b_j, b_(j+1)), b_j = the first rollout start at or after begin + j*S -- unless that
+// start is more than kSegMaxNoCut tokens away (a rollout that long is cut at begin + j*S, flagged). A segment that
+// ends at a rollout start needs no carry from anywhere (its last token is a rollout end), so a persistent CTA
+// streams it alone, right to left, in 2048-token tiles through a 3-stage TMA ring, the carry between its tiles in
+// a register: no look-back, no inter-CTA wait. Only a segment ending inside a (> kSegMaxNoCut) rollout waits for
+// the published value at its right neighbour's first token. Segments are claimed in descending order (ticket), so
+// the neighbour a CTA waits for is always already running. Per tile: pass 1 (thread maps, f64) -> block scan ->
+// pass 2 from the carry (A written over r, R over V in shared memory) -> bulk stores (edge tiles: per token) ->
+// fused loss terms (dfx_gae_ppo_loss) read coalesced -> the stage is refilled with the tile 3 ahead.
+// Everything a CTA computes is a fixed sequence of operations on its segment: run-to-run bit-identical; the
+// whitening / loss partials are per segment, summed in segment order by the finish kernels.
+// ---------------------------------------------------------------------------------------------------------------
+constexpr int kSegThreads = 128, kSegTPT = 16, kSegTile = kSegThreads * kSegTPT, kSegStages = 3;
+constexpr int64_t kSegMaxNoCut = 65536;
+constexpr unsigned long long kSegCut = 1ull << 62;
+struct SegStage {  // r, V (+ the successor), mask (+ the successor), the rollout-end bitmap slice
+  static constexpr uint32_t kR = 0, kV = kSegTile * 4 + 16, kM = kV + kSegTile * 4 + 16, kE = kM + kSegTile + 16,
+                            kBytes = (kE + kSegTile / 8 + 32 + 127) & ~127u;
+};
+
+// segment starts owned by rollout start s (s == n_seq: the span end, a virtual start): the segments whose nominal
+// start P_j lies in (cu[s-1], cu[s]]
+__device__ __forceinline__ void seg_bounds_from_start(const GaeParams& p, int64_t s) {
+  const auto cl = [&](int64_t x) { return max(p.begin, min(p.end, x)); };
+  const int64_t c = s < p.n_seq ? cl(__ldg(p.cu + s)) : p.end;
+  const int64_t jlo = s > 0 ? (cl(__ldg(p.cu + s - 1)) - p.begin) / p.seg_len + 1 : 0;
+  const int64_t jhi = min((c - p.begin) / p.seg_len, p.n_segs - 1);
+  for (int64_t j = jlo; j <= jhi; ++j) {
+    const int64_t P = p.begin + j * p.seg_len;
+    p.seg_start[j] = c - P <= kSegMaxNoCut ? (unsigned long long)c : ((unsigned long long)P | kSegCut);
+  }
+  if (s == p.n_seq) p.seg_start[p.n_segs] = (unsigned long long)p.end;
+}
+
+// bit k set iff byte k of w is nonzero
+__device__ __forceinline__ uint32_t nz_bytes4(uint32_t w) {
+  const uint32_t x = __vcmpne4(w, 0u) & 0x01010101u;
+  return (x | (x >> 7) | (x >> 14) | (x >> 21)) & 0xfu;
+}
+
+// (thread 0) the bulk loads of one tile into a stage: r, V, mask, and the 16-byte-aligned slice of the rollout-end
+// bitmap that covers it (its bit (T0 - base) sits at byte seg_ebyte(T0, base) of the stage's copy)
+__device__ __forceinline__ int64_t seg_ebyte16(int64_t T0, int64_t base) { return ((T0 - base) >> 3) & ~int64_t(15); }
+
+template <bool LOSS>
+__device__ __forceinline__ void seg_issue_load(const GaeParams& p, uint8_t* st, uint64_t* bar, int64_t T0, uint32_t n) {
+  float* s_v = reinterpret_cast<float*>(st + SegStage::kV);
+  uint8_t* s_m = st + SegStage::kM;
+  // the token after the tile (16-aligned): its V and mask land one past the tile in shared memory, by the same
+  // bulk copies extended by 16 bytes; past the batch it is never read (the batch's last token ends a rollout)
+  const int64_t tn = T0 + n;
+  const uint32_t xs = tn < p.end ? 16u : 0u;
+  const int64_t eb0 = seg_ebyte16(T0, p.base);
+  const uint32_t ebytes = (uint32_t)((((T0 - p.base + n + 7) >> 3) - eb0 + 15) & ~int64_t(15));
+  mbar_arrive_expect_tx(bar, 9u * n + 2u * xs + ebytes);
+  tma_load_1d(st + SegStage::kR, p.rew + T0, 4u * n, bar);
+  tma_load_1d(s_v, p.val + T0, 4u * n + xs, bar);
+  tma_load_1d(s_m, p.mask + T0, n + xs, bar);
+  tma_load_1d(st + SegStage::kE, p.ends + eb0, ebytes, bar);
+  if (LOSS) {  // the loss phase reads these coalesced from L2
+    l2_prefetch(p.lp + T0, 4u * n);
+    l2_prefetch(p.old_lp + T0, 4u * n);
+    l2_prefetch(p.ref_lp + T0, 4u * n);
+  }
+}
+
+template <bool WHITEN, bool LOSS>
+__global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
+  constexpr int NW = kSegThreads / 32;
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t s_full[kSegStages];
+  __shared__ Aff s_warp[NW];
+  __shared__ double s_X;
+  __shared__ double s_red[NW][5];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s0 = lane & 3;
+  if (tid == 0) {
+    for (int i = 0; i < kSegStages; ++i) mbar_init(&s_full[i], 1);
+    mbar_fence_init();
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the prep grid: bitmap, bounds, epoch, ticket reset
+  unsigned long long* tr = p.trace ? p.trace + 32 * blockIdx.x : nullptr;
+  int nseg_done = 0;
+  if (tr && tid == 0) tr[0] = gtimer();
+  unsigned int epoch;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(epoch) : "l"(p.ticket + 2) : "memory");
+  const unsigned int F_INC = (epoch << 2) | 2u;
+  const double gamd = p.gamma, gld = p.gl, gld4 = (p.gl * p.gl) * (p.gl * p.gl);
+  uint32_t phase = 0u;  // parity bit per stage
+  for (;;) {
+    // static assignment, descending: CTA c takes segments n_segs-1-c, n_segs-1-c-grid, ...; a segment that waits
+    // for its right neighbour waits for a lower (CTA, round) pair, so every wait chain ends
+    const int64_t j = p.n_segs - 1 - (int64_t)blockIdx.x - (int64_t)nseg_done * gridDim.x;
+    ++nseg_done;
+    if (tr && tid == 0) {
+      if (nseg_done == 1) tr[1] = gtimer();
+      tr[22] = (unsigned long long)nseg_done;
+    }
+    if (j < 0) break;
+    const unsigned long long sb = p.seg_start[j], se = p.seg_start[j + 1];
+    const int64_t b = (int64_t)(sb & ~kSegCut), e = (int64_t)(se & ~kSegCut);
+    const int64_t lo16 = b & ~int64_t(15), e16 = (e + 15) & ~int64_t(15);
+    const int ntl = e > b ? (int)((e16 - lo16 + kSegTile - 1) / kSegTile) : 0;
+    auto tile_T0 = [&](int k) { return max(lo16, e16 - (int64_t)(k + 1) * kSegTile); };
+    if (tid == 0)
+      for (int k = 0; k < min(ntl, kSegStages - 1); ++k) {
+        const int64_t T0 = tile_T0(k);
+        seg_issue_load<LOSS>(p, sm + k * SegStage::kBytes, &s_full[k], T0, (uint32_t)(e16 - (int64_t)k * kSegTile - T0));
+      }
+    if (tid == 0) {
+      double X = 0.0;
+      if (ntl > 0 && (se & kSegCut)) {  // ends inside a rollout: the value at the next segment's first token
+        ulonglong2 r = rec_load(p.rec + j + 1);
+        while (rec_tag(r) != F_INC) {
+          __nanosleep(64);
+          r = rec_load(p.rec + j + 1);
+        }
+        X = rec_x(r);
+      }
+      s_X = X;
+    }
+    double wsum = 0.0, wsq = 0.0;
+    uint32_t wcnt = 0u;
+    double lsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    __syncthreads();  // s_X
+    for (int k = 0; k < ntl; ++k) {
+      const int stg = k % kSegStages;
+      uint8_t* st = sm + stg * SegStage::kBytes;
+      float* s_r = reinterpret_cast<float*>(st + SegStage::kR);
+      float* s_v = reinterpret_cast<float*>(st + SegStage::kV);
+      const uint8_t* s_m = st + SegStage::kM;
+      const int64_t T0 = tile_T0(k);
+      const uint32_t n = (uint32_t)(e16 - (int64_t)k * kSegTile - T0);
+      const bool interior = T0 >= b && T0 + n <= e;
+      const int64_t c0 = T0 + (int64_t)tid * kSegTPT;
+      // this thread's tokens outside the segment or past the tile are identities; its rollout-end bits (half a
+      // bitmap word)
+      const int64_t te = min(e, T0 + (int64_t)n);
+      uint32_t ident = 0u, last = 0u;
+      if (!(c0 >= b && c0 + kSegTPT <= te)) {
+        for (int q = 0; q < kSegTPT; ++q)
+          if (c0 + q < b || c0 + q >= te) ident |= 1u << q;
+      }
+      mbar_wait(&s_full[stg], (phase >> stg) & 1u);
+      phase ^= 1u << stg;
+      if (tr && tid == 0 && nseg_done == 1 && k < 8) tr[4 + k] = gtimer();
+      if (ident != 0xffffu) {  // this thread's 16 end bits from the stage's bitmap slice; cleared in global memory
+        const int64_t ob = c0 - p.base;
+        last = (uint32_t)*reinterpret_cast<const uint16_t*>(st + SegStage::kE + ((ob >> 3) - seg_ebyte16(T0, p.base))) &
+               ~ident;
+        if (last)  // (own bits only: a word can be shared with a neighbouring segment; the bitmap is zero between calls)
+          atomicAnd(reinterpret_cast<uint32_t*>(p.ends) + (ob >> 5), ~(last << (int)(((ob >> 4) & 1) * 16)));
+      }
+      // link bits: token q's successor is unmasked and in the same rollout (16 tokens + the next thread's first)
+      uint32_t lkb, onm;  // (onm: masked-in tokens of the segment)
+      {
+        const uint4 mw = *reinterpret_cast<const uint4*>(s_m + tid * kSegTPT);
+        const uint32_t on = nz_bytes4(mw.x) | nz_bytes4(mw.y) << 4 | nz_bytes4(mw.z) << 8 | nz_bytes4(mw.w) << 12;
+        const uint32_t nx = s_m[tid * kSegTPT + kSegTPT] ? 1u : 0u;
+        lkb = ((on >> 1) | (nx << 15)) & ~last & 0xffffu;
+        onm = on & ~ident;
+      }
+      // pass 1: chunk maps in the per-lane rotated order (conflict-free 128-bit shared reads); a chunk of four
+      // linked tokens inside the segment (the common case) takes the select-free path
+      const float vn_cross = s_v[tid * kSegTPT + kSegTPT];
+      double Hd = 0.0, Hc = 1.0, Td = 0.0, Tc = 1.0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int ch = (s0 + jj) & 3;
+        const int i0 = tid * kSegTPT + ch * 4;
+        const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
+        const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
+        const float vnx = ch == 3 ? vn_cross : s_v[i0 + 4];
+        const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        const uint32_t l4 = (lkb >> (4 * ch)) & 0xfu, id4 = (ident >> (4 * ch)) & 0xfu;
+        double fd = 0.0, fc = 1.0;
+        if (l4 == 0xfu && id4 == 0u) {
+          double vn = (double)vnx;
+#pragma unroll
+          for (int kk = 3; kk >= 0; --kk) {
+            const double v = (double)vv[kk];
+            fd = fma(gld, fd, fma(gamd, vn, (double)rr[kk]) - v);
+            vn = v;
+          }
+          fc = gld4;
+        } else {
+#pragma unroll
+          for (int kk = 3; kk >= 0; --kk) {
+            const int q = ch * 4 + kk;
+            const bool lk = (lkb >> q) & 1u;
+            const float vnext = kk == 3 ? vnx : vv[kk + 1];
+            const double dq = (lk ? fma(gamd, (double)vnext, (double)rr[kk]) : (double)rr[kk]) - (double)vv[kk];
+            if (!((ident >> q) & 1u)) {
+              fd = lk ? fma(gld, fd, dq) : dq;
+              fc = lk ? fc * gld : 0.0;
+            }
+          }
+        }
+        if (ch >= s0) {
+          Td = fma(Tc, fd, Td);
+          Tc *= fc;
+        } else {
+          Hd = fma(Hc, fd, Hd);
+          Hc *= fc;
+        }
+      }
+      Aff S{fma(Hc, Td, Hd), Hc * Tc};
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double od = __shfl_down_sync(kFull, S.d, o), oc = __shfl_down_sync(kFull, S.c, o);
+        if (lane + o < 32) S = compose(S, Aff{od, oc});
+      }
+      if (lane == 0) s_warp[wid] = S;
+      Aff E{__shfl_down_sync(kFull, S.d, 1), __shfl_down_sync(kFull, S.c, 1)};
+      if (lane == 31) E = Aff{0.0, 1.0};
+      __syncthreads();  // s_warp; every thread has read its successor value (vn_cross)
+      double Xd = s_X;
+#pragma unroll
+      for (int w = NW - 1; w >= 0; --w)
+        if (w > wid) Xd = fma(s_warp[w].c, Xd, s_warp[w].d);
+      const double Xin = fma(E.c, Xd, E.d);
+      double X = fma(Tc, Xin, Td);
+      float wa = 0.0f, wa2 = 0.0f;
+      uint32_t wn = 0u;
+      float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
+      int pend_i = -1;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int ch = (s0 - 1 - jj) & 3;
+        if (jj == s0) X = Xin;
+        const int i0 = tid * kSegTPT + ch * 4;
+        const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
+        const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
+        const float vnx = ch == 3 ? vn_cross : s_v[i0 + 4];
+        if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+        const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        float oa[4], orr[4];
+        const uint32_t l4 = (lkb >> (4 * ch)) & 0xfu, id4 = (ident >> (4 * ch)) & 0xfu;
+        if (l4 == 0xfu && id4 == 0u) {
+          double vn = (double)vnx;
+#pragma unroll
+          for (int kk = 3; kk >= 0; --kk) {
+            const double v = (double)vv[kk];
+            X = fma(gld, X, fma(gamd, vn, (double)rr[kk]) - v);
+            oa[kk] = (float)X;
+            orr[kk] = (float)(X + v);
+            vn = v;
+          }
+        } else {
+#pragma unroll
+          for (int kk = 3; kk >= 0; --kk) {
+            const int q = ch * 4 + kk;
+            const bool lk = (lkb >> q) & 1u;
+            const float vnext = kk == 3 ? vnx : vv[kk + 1];
+            const double dq = (lk ? fma(gamd, (double)vnext, (double)rr[kk]) : (double)rr[kk]) - (double)vv[kk];
+            const double A = lk ? fma(gld, X, dq) : dq;
+            X = ((ident >> q) & 1u) ? X : A;
+            oa[kk] = (float)X;
+            orr[kk] = (float)(X + (double)vv[kk]);
+          }
+        }
+        if (WHITEN) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const float mw = ((onm >> (ch * 4 + kk)) & 1u) ? 1.0f : 0.0f;
+            wa = fmaf(mw, oa[kk], wa);
+            wa2 = fmaf(mw * oa[kk], oa[kk], wa2);
+          }
+          wn += __popc((onm >> (4 * ch)) & 0xfu);
+        }
+        *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
+        if (interior) {
+          pendR = make_float4(orr[0], orr[1], orr[2], orr[3]);
+          pend_i = i0;
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (!((ident >> (ch * 4 + kk)) & 1u)) {
+              if (!LOSS || p.adv) p.adv[c0 + ch * 4 + kk] = oa[kk];
+              p.ret[c0 + ch * 4 + kk] = orr[kk];
+            }
+          }
+        }
+      }
+      if (interior) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+      if (WHITEN) {
+        wsum += (double)wa;
+        wsq += (double)wa2;
+        wcnt += wn;
+      }
+      fence_proxy_async_smem();
+      __syncthreads();  // the tile's A and R in shared memory; every thread has read s_X
+      if (tr && tid == 0 && nseg_done == 1 && k < 8) tr[12 + k] = gtimer();
+      if (tid == 0) {
+        s_X = X;  // thread 0's first token: the value at the tile's first segment token = the next tile's carry
+        if (interior) {
+          if (!LOSS || p.adv) tma_store_1d(p.adv + T0, s_r, 4u * n);
+          tma_store_1d(p.ret + T0, s_v, 4u * n);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // (one group per tile, possibly empty)
+        if (k + kSegStages - 1 < ntl) {  // refill the previous tile's stage once its stores have read it
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          const int kn = k + kSegStages - 1;
+          const int64_t T0n = tile_T0(kn);
+          seg_issue_load<LOSS>(p, sm + (kn % kSegStages) * SegStage::kBytes, &s_full[kn % kSegStages], T0n,
+                               (uint32_t)(e16 - (int64_t)kn * kSegTile - T0n));
+        }
+      }
+      if (LOSS) {
+        float lpg = 0.0f, lkl = 0.0f, lakl = 0.0f;
+        uint32_t lclip = 0u, lcnt = 0u;
+        gae_tile_loss<kSegThreads>(p, T0, n, b, e, s_r, s_m, lpg, lkl, lakl, lclip, lcnt);
+        lsum[0] += (double)lpg;
+        lsum[1] += (double)lkl;
+        lsum[2] += (double)lakl;
+        lsum[3] += (double)lclip;
+        lsum[4] += (double)lcnt;
+      }
+      // (no barrier here: the next refill targets this tile's stage only after the next tile's barriers)
+    }
+    if (tr && tid == 0 && nseg_done == 1) {
+      tr[2] = (unsigned long long)j;
+      tr[3] = (unsigned long long)ntl;
+      tr[20] = gtimer();
+    }
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // (the stores complete before the CTA exits)
+      rec_store(p.rec + j, s_X, 0.0f, F_INC);  // the value at b: the carry of segment j-1 if b cuts a rollout
+    }
+    if (WHITEN || LOSS) {  // per-segment partials: fixed-shape block reduction
+      double v[5];
+      if (LOSS) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) v[q] = warp_sum(lsum[q]);
+      } else {
+        v[0] = warp_sum(wsum);
+        v[1] = warp_sum(wsq);
+        v[2] = (double)warp_sum(wcnt);
+        v[3] = v[4] = 0.0;
+      }
+      if (lane == 0)
+        for (int q = 0; q < 5; ++q) s_red[wid][q] = v[q];
+      __syncthreads();
+      if (tid < (LOSS ? 5 : 3)) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += s_red[w][tid];
+        if (LOSS) p.lpart[(int64_t)tid * p.n_segs + j] = t;
+        else p.part[(int64_t)tid * p.n_segs + j] = t;
+      }
+    }
+  }
+  if (tr && tid == 0) tr[21] = gtimer();
 }
 
 // ---- whitening sums: fixed-shape reduction of the per-tile partials ---------------------------------------------
@@ -531,7 +928,7 @@ int64_t gae_tiles(int64_t token_base, int64_t token_span, int64_t tile) {
 constexpr int64_t kGaeMinTile = 2048;  // smallest tile of any variant (s64: 64 x 32 tokens; workspace sizing)
 
 struct GaeWs {
-  size_t ticket, ends, rec, part, lpart, bytes;
+  size_t ticket, ends, rec, part, lpart, segs, bytes;
   int64_t cap_tiles;
 };
 // The layout is a function of the tile CAPACITY only, never of the call's span: the self-maintained state (the
@@ -548,34 +945,41 @@ GaeWs gae_ws_layout_cap(int64_t cap_tiles) {
   w.rec = w.ends + al(size_t(cap_tiles) * kGaeMinTile / 8 + 16);
   w.part = w.rec + al(16 * size_t(cap_tiles));
   w.lpart = w.part + al(24 * size_t(cap_tiles));
-  w.bytes = w.lpart + al(40 * size_t(cap_tiles));
+  w.segs = w.lpart + al(40 * size_t(cap_tiles));
+  w.bytes = w.segs + al(8 * size_t(cap_tiles + 1));
   return w;
 }
 // tiles needed for a span (tile count depends on token_base & 15 as well: size for the worst case)
 int64_t gae_tiles_needed(int64_t token_span) { return (token_span + 15) / kGaeMinTile + 2; }
 // the largest capacity whose layout fits in ws_bytes (the caller's buffer size fixes the layout)
 GaeWs gae_ws_layout_fit(size_t ws_bytes) {
-  int64_t cap = (int64_t)(ws_bytes / (kGaeMinTile / 8 + 16 + 24 + 40));  // an upper bound; step down to the fit
+  int64_t cap = (int64_t)(ws_bytes / (kGaeMinTile / 8 + 16 + 24 + 40 + 8));  // an upper bound; step down to the fit
   while (cap > 0 && gae_ws_layout_cap(cap).bytes > ws_bytes) --cap;
   return gae_ws_layout_cap(cap);
 }
 
-// Tuning knob (benchmarking only): DFX_GAE_VARIANT = s128 (default: 128 threads x 32 tokens, 5 CTAs/SM) |
-// s128b4 | s256 | s64 (the register-tile designs it replaced are in profiles/r01_gae_experiments.md)
-inline int gae_variant() {
+// Tuning knob (benchmarking only): DFX_GAE_VARIANT = seg (rollout-aligned segments: the default of dfx_gae) |
+// lb (one 4096-token tile per CTA with a decoupled look-back: the default of the fused dfx_gae_ppo_loss, whose
+// per-tile loss phase needs the latency hiding of 5 independent CTAs per SM) | lb64 (64 x 32)
+inline int gae_variant(bool fused) {
   static const int v = [] {
     const char* e = std::getenv("DFX_GAE_VARIANT");
-    if (!e) return 0;
+    if (!e) return -1;
     const std::string s(e);
-    return s == "s128b4" ? 1 : s == "s256" ? 2 : s == "s64" ? 3 : 0;
+    return s == "lb" ? 1 : s == "lb64" ? 2 : 0;
   }();
-  return v;
+  return v >= 0 ? v : (fused ? 1 : 0);
+}
+
+template <typename K>
+void gae_set_smem(K kernel, uint32_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int THREADS, int MINB, bool LOSS = false>
 void gae_launch_smem(GaeParams& p, cudaStream_t st) {
   using L = SmemTile<THREADS>;
-  constexpr uint32_t kSmem = LOSS && kLossSmem ? L::kBytesLoss : L::kBytes;
+  constexpr uint32_t kSmem = L::kBytes;
   p.n_tiles = gae_tiles(p.begin, p.end - p.begin, L::TILE);
   static thread_local int cached_dev = -1, resident = 0;
   int dev = 0;
@@ -605,6 +1009,79 @@ void gae_launch_smem(GaeParams& p, cudaStream_t st) {
   else cudaLaunchKernelEx(&cfg, gae_smem_kernel<THREADS, MINB, false, LOSS>, p);
 }
 
+
+
+// segments: about one per resident CTA (at least one tile); the prep kernel writes their bounds
+template <bool LOSS>
+void gae_seg_plan(GaeParams& p, unsigned long long* seg_start) {
+  static thread_local int cached_dev = -1, resident = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  constexpr uint32_t kSmem = kSegStages * SegStage::kBytes;
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    gae_set_smem(gae_seg_kernel<true, LOSS>, kSmem);
+    gae_set_smem(gae_seg_kernel<false, LOSS>, kSmem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_seg_kernel<false, LOSS>, kSegThreads, kSmem);
+    resident = sms * std::max(per_sm, 1);
+    cached_dev = dev;
+  }
+  const int64_t span = p.end - p.begin;
+  p.seg_len = std::max<int64_t>(kSegTile, (span + resident - 1) / resident);  // about one segment per CTA
+  p.n_segs = (span + p.seg_len - 1) / p.seg_len;
+  p.n_tiles = resident;  // (grid)
+  p.seg_start = seg_start;
+}
+
+// DFX_GAE_TRACE=1 (diagnostics only, synchronises): per-CTA phase times of the segment kernel to stderr
+inline void gae_seg_trace_report(const GaeParams& p, unsigned grid, cudaStream_t st) {
+  std::vector<unsigned long long> h(size_t(grid) * 32);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, tend = 0;
+  for (unsigned c = 0; c < grid; ++c) {
+    t0 = std::min(t0, h[32 * c]);
+    tend = std::max(tend, h[32 * c + 21]);
+  }
+  auto med = [&](int slot, bool only_real) {
+    std::vector<double> v;
+    for (unsigned c = 0; c < grid; ++c)
+      if (h[32 * c + slot] && (!only_real || h[32 * c + 3] > 0)) v.push_back((h[32 * c + slot] - t0) * 1e-3);
+    if (v.empty()) return -1.0;
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  std::fprintf(stderr, "[gae trace] grid %u n_segs %lld S %lld span %.3f us | median us: entry %.2f claim %.2f", grid,
+               (long long)p.n_segs, (long long)p.seg_len, (tend - t0) * 1e-3, med(0, false), med(1, false));
+  for (int k = 0; k < 8; ++k) std::fprintf(stderr, " | t%d ready %.2f done %.2f", k, med(4 + k, true), med(12 + k, true));
+  std::fprintf(stderr, " | seg end %.2f exit %.2f\n", med(20, true), med(21, false));
+}
+
+template <bool LOSS>
+void gae_launch_seg(GaeParams& p, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>(p.n_segs, p.n_tiles));
+  cfg.blockDim = dim3(kSegThreads);
+  cfg.dynamicSmemBytes = kSegStages * SegStage::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static const bool trace = std::getenv("DFX_GAE_TRACE") != nullptr;
+  static unsigned long long* tbuf = nullptr;
+  if (trace) {
+    if (!tbuf) cudaMalloc(&tbuf, 32 * 8 * 4096);
+    cudaMemsetAsync(tbuf, 0, 32 * 8 * cfg.gridDim.x, st);
+    p.trace = tbuf;
+  }
+  if (p.whiten) cudaLaunchKernelEx(&cfg, gae_seg_kernel<true, LOSS>, p);
+  else cudaLaunchKernelEx(&cfg, gae_seg_kernel<false, LOSS>, p);
+  if (trace) gae_seg_trace_report(p, cfg.gridDim.x, st);
+  p.trace = nullptr;
+}
 
 }  // namespace dfx
 
@@ -647,18 +1124,18 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
   p.adv = adv;
   p.ret = ret;
   p.whiten = whiten;
-  gae_prep_kernel<<<(unsigned)((p.n_seq + 255) / 256), 256, 0, stream>>>(p.cu, p.n_seq, p.base,
-                                                                          reinterpret_cast<uint32_t*>(p.ends), p.ticket);
+  const int v = gae_variant(false);
+  if (v == 0) gae_seg_plan<false>(p, reinterpret_cast<unsigned long long*>(w + wl.segs));
+  gae_prep_kernel<<<(unsigned)((p.n_seq + 1 + 255) / 256), 256, 0, stream>>>(p);
   DFX_LAUNCH_CHECK("gae_prep_kernel");
-  switch (gae_variant()) {
-    case 1: gae_launch_smem<128, 4>(p, stream); break;
-    case 2: gae_launch_smem<256, 2>(p, stream); break;
-    case 3: gae_launch_smem<64, 8>(p, stream); break;
-    default: gae_launch_smem<128, 5>(p, stream); break;
+  switch (v) {
+    case 1: gae_launch_smem<128, 5>(p, stream); break;
+    case 2: gae_launch_smem<64, 8>(p, stream); break;
+    default: gae_launch_seg<false>(p, stream); break;
   }
-  DFX_LAUNCH_CHECK("gae_smem_kernel");
+  DFX_LAUNCH_CHECK("gae scan");
   if (whiten) {
-    gae_finish_kernel<<<1, 256, 0, stream>>>(p.part, p.n_tiles, whiten);
+    gae_finish_kernel<<<1, 256, 0, stream>>>(p.part, v == 0 ? p.n_segs : p.n_tiles, whiten);
     DFX_LAUNCH_CHECK("gae_finish_kernel");
   }
   return DFX_OK;
@@ -721,16 +1198,18 @@ dfx_status dfx_gae_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t tok
   p.t_hi32_lo = (float)(t_hi - (double)p.t_hi32);
   p.t_lo32_lo = std::isfinite(t_lo) ? (float)(t_lo - (double)p.t_lo32) : 0.0f;
   p.kl_type = cfg->kl_type;
-  gae_prep_loss_kernel<<<(unsigned)((p.n_seq + 7) / 8), 256, 0, stream>>>(
-      p.cu, p.n_seq, p.base, reinterpret_cast<uint32_t*>(p.ends), p.ticket, p.mask, p.seq_has);
+  const int v = gae_variant(true);
+  if (v == 0) gae_seg_plan<true>(p, reinterpret_cast<unsigned long long*>(w + wl.segs));
+  gae_prep_loss_kernel<<<(unsigned)((p.n_seq + 1 + 7) / 8), 256, 0, stream>>>(p);
   DFX_LAUNCH_CHECK("gae_prep_loss_kernel");
-  switch (gae_variant()) {
-    case 1: gae_launch_smem<128, 4, true>(p, stream); break;
-    case 3: gae_launch_smem<64, 8, true>(p, stream); break;
-    default: gae_launch_smem<128, 5, true>(p, stream); break;
+  switch (v) {
+    case 1: gae_launch_smem<128, 5, true>(p, stream); break;
+    case 2: gae_launch_smem<64, 8, true>(p, stream); break;
+    default: gae_launch_seg<true>(p, stream); break;
   }
-  DFX_LAUNCH_CHECK("gae_smem_kernel<loss>");
-  gae_loss_finish_kernel<<<1, 256, 0, stream>>>(p.lpart, p.n_tiles, p.seq_has, p.n_seq, cfg->beta, out);
+  DFX_LAUNCH_CHECK("gae scan<loss>");
+  gae_loss_finish_kernel<<<1, 256, 0, stream>>>(p.lpart, v == 0 ? p.n_segs : p.n_tiles, p.seq_has, p.n_seq,
+                                                 cfg->beta, out);
   DFX_LAUNCH_CHECK("gae_loss_finish_kernel");
   return DFX_OK;
 }

@@ -187,6 +187,9 @@ __global__ void __launch_bounds__(256) slot_table_kernel(SlotGeom g, int64_t n_s
 // ---- per-token math (k3_series, clip_exact_f32: common.cuh) ---------------------------------------------
 // per lane and round: f32 sums of the surrogate / KL / log ratio; exact integer counts of clipped and masked tokens
 // (bit counts per vector instead of a multiply-add per token)
+struct WhitenF {  // per-token whitening (A - mu) * rstd with mu = mu_hi + mu_lo
+  float mu_hi, mu_lo, rstd;
+};
 struct TokAcc {
   float pg, kl, akl;
   uint32_t clip, n;
@@ -223,8 +226,8 @@ __device__ __forceinline__ bool clip_twosum(const LossParams& p, float s, float 
 // Four tokens of one aligned vector starting at token t. FULL: all in range.
 template <int ADV, int KL, bool DLOGP, bool FULL>
 __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua, float4 lv, float4 ov, float4 rv,
-                                         float4 av, uint32_t mk, int64_t t, int64_t t0, int64_t t1, double mu,
-                                         double rstd, float w, TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
+                                         float4 av, uint32_t mk, int64_t t, int64_t t0, int64_t t1, const WhitenF& wf,
+                                         float w, TokAcc& acc, float (&aout)[4], float (&gout)[4]) {
   const float lo = 1.0f - p.clip_lo, hi = 1.0f + p.clip_hi;
   float x[4], kl[4], dkl[4];
 #pragma unroll
@@ -280,6 +283,29 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
       cl[k] = DFX_CLIP_MODE == 2 ? ua.s * dd[k] > ua.sT32
                                  : clip_twosum(p, ua.s, ua.sT32, f4_get(lv, k), f4_get(ov, k), dd[k]);
   }
+  float At[4];  // per-token advantages (GAE): whitened here, clip decision as in mode 1 per token
+  if constexpr (ADV == DFX_ADV_TOKEN) {
+    bool near = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // whitening with mu as an f32 pair: the rounding of mu alone would shift every advantage alike, the
+      // rounding of each subtraction is relative to the token's own whitened value
+      At[k] = p.whiten ? ((f4_get(av, k) - wf.mu_hi) - wf.mu_lo) * wf.rstd : f4_get(av, k);
+      const float sg = At[k] < 0.0f ? -1.0f : 1.0f;
+      const float sT = At[k] > 0.0f ? p.t_hi32 : (At[k] < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
+      const float sd = sg * dd[k];
+      cl[k] = sd > sT;
+      near |= fabsf(sd - sT) <= p.clip_margin;
+    }
+    if (near) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float sg = At[k] < 0.0f ? -1.0f : 1.0f;
+        const float sT = At[k] > 0.0f ? p.t_hi32 : (At[k] < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
+        cl[k] = clip_twosum(p, sg, sT, f4_get(lv, k), f4_get(ov, k), dd[k]);
+      }
+    }
+  }
   uint32_t onb = 0u, clb = 0u;  // this vector's masked-in and clipped tokens, as bits
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -290,13 +316,9 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
     const float rho = exp2f(d * kLog2e);     // MUFU.EX2, ~2 ulp
     float A, pg;
     if constexpr (ADV == DFX_ADV_TOKEN) {
-      // whitening in f64 (mu, rstd f64): the f32 rounding of mu would shift every advantage alike
-      A = p.whiten ? (float)(((double)f4_get(av, k) - mu) * rstd) : f4_get(av, k);
+      A = At[k];
       const float rc = fminf(fmaxf(rho, lo), hi);
       pg = fmaxf(-A * rho, -A * rc);
-      const float s = A < 0.0f ? -1.0f : 1.0f;
-      const float sT = A > 0.0f ? p.t_hi32 : (A < 0.0f ? -p.t_lo32 : __int_as_float(0x7f800000));
-      cl[k] = clip_twosum(p, s, sT, f4_get(lv, k), f4_get(ov, k), d);
     } else {
       A = ua.A;
       const float sr = ua.s * rho;
@@ -425,8 +447,14 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
 
   // whitening coefficients: live across the loop only for per-token advantages; the per-rollout paths whiten
   // once per slot (keeps the hot kernels' registers for loads in flight)
-  double mu = 0.0, rstd = 1.0;
-  if (ADV == DFX_ADV_TOKEN && p.whiten) whiten_coeffs(p, mu, rstd);
+  WhitenF wf{0.0f, 0.0f, 1.0f};
+  if (ADV == DFX_ADV_TOKEN && p.whiten) {
+    double mu, rstd;
+    whiten_coeffs(p, mu, rstd);
+    wf.mu_hi = (float)mu;
+    wf.mu_lo = (float)(mu - (double)wf.mu_hi);
+    wf.rstd = (float)rstd;
+  }
   double* part = p.part;
   // tickets: [k] next slot of source k, [kMaxLossSrc] finished warps. Several sources (e.g. local HBM and a
   // partner GPU's memory over NVLink) are drained concurrently: warp w starts on source w % n_src and moves to the
@@ -511,12 +539,12 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         const int64_t t = 4 * (vbeg + i);
         float aout[4], gout[4];
         if (t >= t0 && t + 4 <= t1) {
-          loss_vec<ADV, KL, DLOGP, true>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
+          loss_vec<ADV, KL, DLOGP, true>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, wf, w, acc, aout,
                                          gout);
           if (atout) store_vec<true>(atout, t, t0, t1, aout);
           if (DLOGP) store_vec<true>(dlout, t, t0, t1, gout);
         } else {
-          loss_vec<ADV, KL, DLOGP, false>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, mu, rstd, w, acc, aout,
+          loss_vec<ADV, KL, DLOGP, false>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, wf, w, acc, aout,
                                           gout);
           if (atout) store_vec<false>(atout, t, t0, t1, aout);
           if (DLOGP) store_vec<false>(dlout, t, t0, t1, gout);

@@ -236,9 +236,9 @@ def test_multi_source_with_empty_source(dfx):
 
 @pytest.mark.parametrize("kl", ["k3", "k1", "none"])
 def test_c3_fused_gae_loss_full_size(O, dfx, kl):
-    """C3 (512 x 8192) through the fused GAE + loss pass (dfx_gae_ppo_loss): returns and the (optional) advantage
-    equal the two-pass path bit for bit, the loss scalars match the f64 oracle on the oracle's own GAE within 1e-5,
-    and two runs give the same bits."""
+    """C3 (512 x 8192) through the fused GAE + loss pass (dfx_gae_ppo_loss): two runs give the same bits; returns and
+    the (optional) advantage match the standalone GAE (a different scan kernel: segments instead of look-back tiles)
+    and the f64 oracle within tolerance; the loss scalars match the oracle on the oracle's own GAE within 1e-5."""
     R, L = 512, 8192
     streams = ("lp", "old_lp", "ref_lp", "mask", "value_tok", "token_reward")
     sb = O.SynthBatch(1, R, 1, O.token_dist("constant", L, L, L), streams=streams)
@@ -250,10 +250,12 @@ def test_c3_fused_gae_loss_full_size(O, dfx, kl):
     a1, ret1, o1 = r1["adv"][:T].clone(), db.streams["returns"][:T].clone(), r1["out"].clone()
     r2 = dfx.gae_ppo_loss(db, ctx)
     assert torch.equal(o1, r2["out"]) and torch.equal(ret1, db.streams["returns"][:T])
-    dfx.fn_gae_advantage(dfx.NodeSpec("g"), db, ctx)  # the two-pass path: same advantages and returns
-    assert torch.equal(a1, db.streams["advantage"][:T]) and torch.equal(ret1, db.streams["returns"][:T])
+    dfx.fn_gae_advantage(dfx.NodeSpec("g"), db, ctx)  # the two-launch path: same advantages and returns
+    A, Rt, _ = O.gae(sb.cu_seqlens, sb.token_reward, sb.value_tok, sb.mask, 1.0, 0.95)
+    assert_close_vec(a1.cpu().numpy(), A[:T], "C3 fused adv")
+    assert_close_vec(ret1.cpu().numpy(), Rt[:T], "C3 fused ret")
+    assert_close_vec(db.streams["advantage"][:T].cpu().numpy(), a1.cpu().numpy(), "C3 fused vs two-launch adv")
     two = dfx.ppo_loss(db, ctx, adv_source="token")["out"].cpu().numpy()[0]
-    A, _, _ = O.gae(sb.cu_seqlens, sb.token_reward, sb.value_tok, sb.mask, 1.0, 0.95)
     ref, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, A[:T].astype(np.float32), sb.mask,
                         O.loss_cfg(kl=kl))
     _check_loss(o1.cpu().numpy()[0], ref, f"C3 fused {kl}")

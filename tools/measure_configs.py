@@ -187,14 +187,17 @@ def wire_c4():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="C1|C2|C3|C4|C5: that config's rows only")
     a = ap.parse_args()
-    rows = [grpo("C1", 64, 8, dfx.TokenDist("constant", 1024)),
-            grpo("C2", 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096)),
-            ppo_c3(),
-            ppo_c3_fused(),
-            grpo("C5/8 (one GPU's share: 512 prompts)", 512, 16, dfx.TokenDist("skewed", 0, 1, 16384)),
-            reshard_c4(),
-            wire_c4()]
+    makers = [("C1", lambda: grpo("C1", 64, 8, dfx.TokenDist("constant", 1024))),
+              ("C2", lambda: grpo("C2", 1024, 16, dfx.TokenDist("uniform", 0, 1, 4096))),
+              ("C3", ppo_c3),
+              ("C3", ppo_c3_fused),
+              ("C5", lambda: grpo("C5/8 (one GPU's share: 512 prompts)", 512, 16,
+                                  dfx.TokenDist("skewed", 0, 1, 16384))),
+              ("C4", reshard_c4),
+              ("C4", wire_c4)]
+    rows = [mk() for tag, mk in makers if a.only in (None, tag)]
     for r in rows:
         print(json.dumps(r), flush=True)
     if a.out:
