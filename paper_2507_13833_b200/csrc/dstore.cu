@@ -300,6 +300,7 @@ constexpr uint64_t kPullChunk = 1ull << 17;
 struct PullList {
   int n;
   uint64_t dst[kPullRuns], src[kPullRuns], bytes[kPullRuns], chunk0[kPullRuns + 1];
+  uint32_t cta0[kPullRuns + 1];  // CTAs [cta0[r], cta0[r+1]) pull run r
 };
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
@@ -308,15 +309,20 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
                : "l"(p));
   return r;
 }
-__global__ void __launch_bounds__(512) peer_pull_kernel(const PullList c, uint64_t n_chunks) {
-  for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    int lo = 0, hi = c.n;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (c.chunk0[mid] <= ch) lo = mid;
-      else hi = mid;
-    }
-    const uint64_t off = (ch - c.chunk0[lo]) * kPullChunk;
+// Every run (one producer range on one peer) gets its own share of the CTAs, proportional to its size, so all
+// peers are read at once (at N = 4 a GPU pulls from three peers; taking the runs one after the other leaves the
+// links to the other two idle and caps the pull at one pair's rate).
+__global__ void __launch_bounds__(512) peer_pull_kernel(const PullList c) {
+  int lo = 0, hi = c.n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (c.cta0[mid] <= blockIdx.x) lo = mid;
+    else hi = mid;
+  }
+  const uint32_t nc = c.cta0[lo + 1] - c.cta0[lo];
+  const uint64_t nch = c.chunk0[lo + 1] - c.chunk0[lo];
+  for (uint64_t ch = blockIdx.x - c.cta0[lo]; ch < nch; ch += nc) {
+    const uint64_t off = ch * kPullChunk;
     const uint64_t n = min(kPullChunk, c.bytes[lo] - off);
     uint8_t* dst = reinterpret_cast<uint8_t*>(c.dst[lo]) + off;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(c.src[lo]) + off;
@@ -340,13 +346,15 @@ __global__ void __launch_bounds__(512) peer_pull_kernel(const PullList c, uint64
 }
 
 dfx_status peer_pull(const std::vector<uint64_t>& dst, const std::vector<uint64_t>& src,
-                     const std::vector<uint64_t>& bytes, cudaStream_t st) {
-  static const int ctas_per_sm = [] {
-    // 2 x 512 threads per SM: enough bytes in flight to saturate NVLink, and room on every SM for the unpack and
-    // local copies running concurrently on the side stream
+                     const std::vector<uint64_t>& bytes, int n_peers, cudaStream_t st) {
+  // 512-thread CTAs per SM: 2 when reading one peer, 1 when reading several at once -- measured (C4, bench.py):
+  // N = 2 0.614 (2) vs 0.60 (1) of 770 GB/s, N = 4 0.64 (1) vs 0.57 (2) vs 0.556 (3); both leave room on every SM
+  // for the unpack and local copies running concurrently on the side stream
+  static const int env_cps = [] {
     const char* e = std::getenv("DFX_PULL_CTAS_PER_SM");  // benchmarking knob
-    return e ? std::max(1, std::atoi(e)) : 2;
+    return e ? std::max(1, std::atoi(e)) : 0;
   }();
+  const int ctas_per_sm = env_cps ? env_cps : (n_peers > 1 ? 1 : 2);
   for (size_t i0 = 0; i0 < bytes.size(); i0 += kPullRuns) {
     PullList c{};
     uint64_t chunks = 0;
@@ -361,8 +369,15 @@ dfx_status peer_pull(const std::vector<uint64_t>& dst, const std::vector<uint64_
     }
     if (!c.n) continue;
     c.chunk0[c.n] = chunks;
-    const unsigned grid = unsigned(std::min<uint64_t>(chunks, uint64_t(148) * ctas_per_sm));
-    peer_pull_kernel<<<grid, 512, 0, st>>>(c, chunks);
+    const uint64_t target = std::min<uint64_t>(chunks, uint64_t(148) * ctas_per_sm);
+    uint32_t ctas = 0;
+    for (int r = 0; r < c.n; ++r) {  // CTAs in proportion to the run's chunks (at least one, at most its chunks)
+      const uint64_t cr = c.chunk0[r + 1] - c.chunk0[r];
+      c.cta0[r] = ctas;
+      ctas += uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(cr, (cr * target + chunks / 2) / chunks)));
+    }
+    c.cta0[c.n] = ctas;
+    peer_pull_kernel<<<ctas, 512, 0, st>>>(c);
     DFX_LAUNCH_CHECK("peer_pull_kernel");
   }
   return DFX_OK;
@@ -903,6 +918,7 @@ dfx_status run_exchange(dfx_dstore* s, const StageCfg& c, uint32_t to_dp, uint32
   // ---- token streams: local copies (side stream) overlapping the remote transfers (main stream) ----
   std::vector<uint64_t> cp_dst, cp_src, cp_n;     // local segments (SM copy kernel)
   std::vector<uint64_t> rp_dst, rp_src, rp_n;     // remote segments, pull transport
+  std::set<int> pull_peers;                        // the ranks they come from
   auto push_merged = [](std::vector<uint64_t>& D, std::vector<uint64_t>& S_, std::vector<uint64_t>& N, uint64_t d,
                         uint64_t src, uint64_t n) {
     if (!N.empty() && D.back() + N.back() == d && S_.back() + N.back() == src) {
@@ -920,6 +936,7 @@ dfx_status run_exchange(dfx_dstore* s, const StageCfg& c, uint32_t to_dp, uint32
       if (sg.n_tok == 0) continue;
       const bool here = src_rank[sg.src] == me;
       if (!here && s->transport != DFX_TRANSPORT_PULL) continue;
+      if (!here) pull_peers.insert(src_rank[sg.src]);
       const SrcArrays& a = src_of(sg.src);
       for (int k = 0; k < s->n_streams; ++k) {
         const uint64_t n = uint64_t(sg.n_tok) * s->esz[k];
@@ -963,7 +980,7 @@ dfx_status run_exchange(dfx_dstore* s, const StageCfg& c, uint32_t to_dp, uint32
   cudaEvent_t t_pull = trace_mark(s);
   if (!rp_n.empty()) {
     if (pull_sm) {
-      dfx_status stt = peer_pull(rp_dst, rp_src, rp_n, st);
+      dfx_status stt = peer_pull(rp_dst, rp_src, rp_n, int(pull_peers.size()), st);
       if (stt) return stt;
     } else {
       // the runs spread over several streams, so several copy engines pull concurrently (one queue would run
