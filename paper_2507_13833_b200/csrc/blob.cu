@@ -27,6 +27,7 @@ struct BlobParams {
   int64_t n_records, n_rollouts;
   const uint64_t* ids;
   const int32_t* group_off;
+  const int32_t* roll_group;  // nullable: the record of each rollout (else a binary search over group_off)
   const int64_t* cu;
   const uint32_t* tok_count;  // nullable: cu[s+1] - cu[s]
   int n_streams;
@@ -52,27 +53,47 @@ __device__ __forceinline__ void put_le(uint8_t* p, uint64_t v, int n) {
 // Copy n bytes src -> dst (any alignment) with the block's threads. The 16-byte-aligned interior of dst is written
 // with 128-bit stores, each assembled from five aligned 32-bit source words with funnel shifts; the bytes before
 // and after it byte by byte (they may share a word with a neighbouring writer).
-__device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+__device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, uint64_t n, uint32_t tid,
+                                           uint32_t nthr) {
   if (n == 0) return;
   const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst), d1 = d0 + n;
   const uintptr_t a0 = (d0 + 15) & ~uintptr_t(15), a1 = d1 & ~uintptr_t(15);
   if (a1 <= a0) {  // no whole aligned 16-byte unit
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    for (uint64_t i = tid; i < n; i += nthr) dst[i] = src[i];
     return;
   }
   const uint64_t head = a0 - d0, tail = d1 - a1;
-  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
-  if (threadIdx.x < tail) dst[n - tail + threadIdx.x] = src[n - tail + threadIdx.x];
+  if (tid < head) dst[tid] = src[tid];
+  if (tid < tail) dst[n - tail + tid] = src[n - tail + tid];
   // unit u covers source bytes [head + 16u, head + 16u + 16)
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src + head);
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
   const uint32_t sh = uint32_t(sa & 3u) * 8u;
   uint4* dv = reinterpret_cast<uint4*>(a0);
   const uint64_t nu = (a1 - a0) / 16;
-  for (uint64_t u = threadIdx.x; u < nu; u += blockDim.x) {
-    const uint32_t* w = sw + 4 * u;
-    const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
-    const uint32_t w4 = sh ? __ldg(w + 4) : 0u;
+  // four units per thread in flight (all loads issued before the first store)
+  constexpr int kU = 4;
+  uint64_t u = tid;
+  for (; u + (kU - 1) * nthr < nu; u += kU * nthr) {
+    uint32_t w[kU][5];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const uint32_t* q = sw + 4 * (u + j * nthr);
+      w[j][0] = __ldg(q);
+      w[j][1] = __ldg(q + 1);
+      w[j][2] = __ldg(q + 2);
+      w[j][3] = __ldg(q + 3);
+      w[j][4] = sh ? __ldg(q + 4) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j)
+      dv[u + j * nthr] = make_uint4(__funnelshift_r(w[j][0], w[j][1], sh), __funnelshift_r(w[j][1], w[j][2], sh),
+                                          __funnelshift_r(w[j][2], w[j][3], sh), __funnelshift_r(w[j][3], w[j][4], sh));
+  }
+  for (; u < nu; u += nthr) {
+    const uint32_t* q = sw + 4 * u;
+    const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3);
+    const uint32_t w4 = sh ? __ldg(q + 4) : 0u;
     dv[u] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
                        __funnelshift_r(w3, w4, sh));
   }
@@ -88,7 +109,7 @@ __global__ void __launch_bounds__(256) serialize_kernel(BlobParams p) {
     int64_t mlen = 4;
     if (p.meta) {
       mlen = p.meta_off[b + 1] - p.meta_off[b];
-      block_copy(o + 8, p.meta + p.meta_off[b], uint64_t(mlen));
+      block_copy(o + 8, p.meta + p.meta_off[b], uint64_t(mlen), threadIdx.x, blockDim.x);
     }
     if (threadIdx.x == 0) {
       put_le(o, p.ids[b], 8);
@@ -100,14 +121,18 @@ __global__ void __launch_bounds__(256) serialize_kernel(BlobParams p) {
   // rollout b: its record by a binary search over group_off, then its offset in O(1)
   __shared__ int64_t s_rec;
   if (threadIdx.x == 0) {
-    int64_t lo = 0, hi = p.n_records;  // last record with group_off[r] <= b
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (p.group_off[mid] <= b) lo = mid;
-      else hi = mid;
+    if (p.roll_group) {
+      s_rec = p.roll_group[b];
+    } else {
+      int64_t lo = 0, hi = p.n_records;  // last record with group_off[r] <= b
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (p.group_off[mid] <= b) lo = mid;
+        else hi = mid;
+      }
+      while (lo + 1 < p.n_records && p.group_off[lo + 1] <= b) ++lo;  // skip empty records
+      s_rec = lo;
     }
-    while (lo + 1 < p.n_records && p.group_off[lo + 1] <= b) ++lo;  // skip empty records
-    s_rec = lo;
   }
   __syncthreads();
   const int64_t r = s_rec;
@@ -123,10 +148,15 @@ __global__ void __launch_bounds__(256) serialize_kernel(BlobParams p) {
     put_le(o, p.tok_count ? p.tok_count[b] : uint32_t(L), 4);
     put_le(o + 4, plen, 8);
   }
-  uint64_t po = 12;
-  for (int k = 0; k < p.n_streams; ++k) {
-    block_copy(o + po, p.streams[k] + uint64_t(t0) * p.esz[k], uint64_t(L) * p.esz[k]);
-    po += uint64_t(L) * p.esz[k];
+  // the streams are copied concurrently: warp w copies stream w % n_streams (with the other warps of that stream),
+  // so the rollout's loads are in flight together instead of one stream after the other
+  if (p.n_streams > 0) {
+    const int ns = p.n_streams, w = int(threadIdx.x >> 5), nw = int(blockDim.x >> 5);
+    const int k = w % ns, cnt = (nw - k + ns - 1) / ns;
+    uint64_t po = 12;
+    for (int j = 0; j < k; ++j) po += uint64_t(L) * p.esz[j];
+    block_copy(o + po, p.streams[k] + uint64_t(t0) * p.esz[k], uint64_t(L) * p.esz[k],
+               uint32_t(w / ns) * 32u + (threadIdx.x & 31u), uint32_t(cnt) * 32u);
   }
   uint8_t* c = o + 12 + plen;
   if (threadIdx.x == 0) put_le(c, uint64_t(p.n_ch), 4);
@@ -181,6 +211,7 @@ dfx_status dfx_serialize_records(const dfx_packed* b, const uint64_t* ids, const
   p.n_rollouts = b->n_rollouts;
   p.ids = ids;
   p.group_off = b->group_off;
+  p.roll_group = b->roll_group;
   p.cu = b->cu_seqlens;
   p.tok_count = tok_count;
   p.n_streams = n_streams;

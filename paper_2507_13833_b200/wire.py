@@ -34,6 +34,15 @@ def serialize(batch: PackedBatch, streams=PAYLOAD_STREAMS, channels=None, meta_b
               meta_off: np.ndarray | None = None, tok_count: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Device blob (uint8 tensor) of the batch's records. channels: names to write (default: all rollout
     channels, sorted like std::map); meta_blob/meta_off: per-record pre-serialized meta sections (host)."""
+    run, out = serialize_prepared(batch, streams, channels, meta_blob, meta_off, tok_count)
+    run(out, stream)
+    return out
+
+
+def serialize_prepared(batch: PackedBatch, streams=PAYLOAD_STREAMS, channels=None, meta_blob=None, meta_off=None,
+                       tok_count=None):
+    """The host plan and device arguments of serialize(), once: returns (run, out) where run(out, stream=None)
+    launches only the device serializer into `out` (repeatable; e.g. for timing the kernel alone)."""
     L = _declare()
     batch.ensure_host_meta()
     dev = batch.device
@@ -66,13 +75,15 @@ def serialize(batch: PackedBatch, streams=PAYLOAD_STREAMS, channels=None, meta_b
     sptr = (C.c_void_p * max(1, len(streams)))(*[batch.streams[k].data_ptr() for k in streams])
     cptr = (C.c_void_p * max(1, len(names)))(*[batch.channels[n].data_ptr() for n in names])
     st = batch.struct()
-    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    _abi.check(L.dfx_serialize_records(C.byref(st), _ptr(batch.ids), _ptr(tok_count), len(streams),
-                                       C.cast(sptr, C.c_void_p), C.cast(esz, C.c_void_p), len(names),
-                                       C.cast(cnames, C.c_void_p), C.cast(cptr, C.c_void_p), _ptr(d_meta),
-                                       _ptr(d_moff), _ptr(d_rec_off), _ptr(out), s))
     out._keep = (d_rec_off, d_meta, d_moff)
-    return out
+
+    def run(dst, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        _abi.check(L.dfx_serialize_records(C.byref(st), _ptr(batch.ids), _ptr(tok_count), len(streams),
+                                           C.cast(sptr, C.c_void_p), C.cast(esz, C.c_void_p), len(names),
+                                           C.cast(cnames, C.c_void_p), C.cast(cptr, C.c_void_p), _ptr(d_meta),
+                                           _ptr(d_moff), _ptr(d_rec_off), _ptr(dst), s))
+    return run, out
 
 
 def deserialize(blob: np.ndarray, streams=(("token_id", torch.int32), ("lp", torch.float32), ("old_lp", torch.float32),
