@@ -15,6 +15,9 @@
 #ifndef DFX_CLIP_MODE
 #define DFX_CLIP_MODE 1
 #endif
+#ifndef DFX_LOSS_PF
+#define DFX_LOSS_PF 1  // L2 bulk prefetch of each claimed slot's streams (C2: 0.1065 -> 0.1034 ms)
+#endif
 #ifndef DFX_TOKEN_MINB
 #define DFX_TOKEN_MINB 2
 #endif
@@ -517,6 +520,18 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     float* const atout = S.adv_tok_out;
     float* const dlout = S.dlogp;
     constexpr int kUnroll = UNROLL;
+#if DFX_LOSS_PF
+    if (lane == 0 && nvec > 32 * kUnroll) {  // the slot's streams into L2 at once (more bytes in flight per warp)
+      const uint32_t fb = (uint32_t)nvec * 16u;
+      l2_prefetch(lp0, fb);
+      l2_prefetch(ol0, fb);
+      l2_prefetch(rf0, fb);
+      if (ADV == DFX_ADV_TOKEN) l2_prefetch(ad0, fb);
+      const uintptr_t m0 = reinterpret_cast<uintptr_t>(mk0) & ~uintptr_t(15);
+      l2_prefetch(reinterpret_cast<const void*>(m0),
+                  (uint32_t)((reinterpret_cast<uintptr_t>(mk0) + 4u * (uint32_t)nvec - m0 + 15u) & ~uintptr_t(15)));
+    }
+#endif
     for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
       float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
       uint32_t mk[kUnroll];
