@@ -206,9 +206,10 @@ __device__ __forceinline__ bool slot_unit(const SlotGeom& g, int64_t u, int lane
 }
 
 // Host: window size of the streaming kernels, a function of the token span only (the workspace sizing and the
-// launch must agree): 2048-token windows. Measured on B200: shorter windows lose more to per-slot setup (search +
-// reduction + partials) than they gain in balance -- at C2's 33.5M tokens and also at C3's 4.2M (2048 windows for
-// ~3.5k resident warps; 512-token windows made the C3 step 20% slower, profiles/r02_clip_sweep2.log).
+// launch must agree): 2048-token windows, 1024 for spans of 7.3M..21.8M tokens. Measured on B200: shorter
+// windows lose more to per-slot setup (claim + table load + reduction + partials) than they gain in balance at C2's
+// 33.5M tokens (1024: 0.81 vs 2048: 0.843 of HBM), and gain at C5's 16.9M (0.7555 vs 0.7303); 512-token windows
+// made the C3 step 20% slower (profiles/r02_clip_sweep2.log).
 // Benchmarking knobs: DFX_SLOT_SHIFT forces the window; DFX_SLOT_TARGET=k halves it until there are k windows per
 // resident warp.
 inline int slot_shift(int64_t token_span) {
@@ -223,9 +224,16 @@ inline int slot_shift(int64_t token_span) {
     const int v = e ? std::atoi(e) : 0;
     return int64_t(v >= 1 && v <= 64 ? v : 0) * 148 * 24;
   }();
-  int sh = 11;
-  while (target && sh > 8 && (token_span >> sh) < target) --sh;
-  return sh;
+  if (target) {
+    int sh = 11;
+    while (sh > 8 && (token_span >> sh) < target) --sh;
+    return sh;
+  }
+  // 2..6k tokens per resident warp (3 x 8 warps on 148 SMs): 1024-token windows, so the last windows are short
+  // enough to balance (C5 per-GPU share, 16.9M tokens: 0.73 -> 0.76 of HBM). Above (C2, 33.5M) 2048 stays best;
+  // below (C3, 4.2M) the doubled slot table and partials cost more than the balance gains (step +9%).
+  const int64_t per_warp = token_span / (int64_t(148) * 24);
+  return per_warp >= 2048 && per_warp < 6144 ? 10 : 11;
 }
 
 // Host: number of slots for n_seq rollouts spanning token_span tokens.

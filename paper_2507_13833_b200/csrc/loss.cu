@@ -16,7 +16,10 @@
 #define DFX_CLIP_MODE 1
 #endif
 #ifndef DFX_LOSS_PF
-#define DFX_LOSS_PF 1  // L2 bulk prefetch of each claimed slot's streams (C2: 0.1065 -> 0.1034 ms)
+// (kernel-variant sweeps) L2 bulk prefetch of each claimed slot's streams. Measured at C2: the loss launch drops
+// from 0.1065 to 0.1034 ms, but the step only by 0.5%: the prefetches still in flight when the kernel retires slow
+// the next kernels down, so the launch time overstates the gain. Off.
+#define DFX_LOSS_PF 0
 #endif
 #ifndef DFX_TOKEN_MINB
 #define DFX_TOKEN_MINB 2
@@ -521,12 +524,13 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     float* const dlout = S.dlogp;
     constexpr int kUnroll = UNROLL;
 #if DFX_LOSS_PF
-    if (lane == 0 && nvec > 32 * kUnroll) {  // the slot's streams into L2 at once (more bytes in flight per warp)
+    // the slot's streams into L2 at once (more bytes in flight per warp than its registers hold). Not on the
+    // per-token-advantage path: its C3-size working set is L2-resident and the prefetches cost 5 us per step
+    if (ADV != DFX_ADV_TOKEN && lane == 0 && nvec > 32 * kUnroll) {
       const uint32_t fb = (uint32_t)nvec * 16u;
       l2_prefetch(lp0, fb);
       l2_prefetch(ol0, fb);
       l2_prefetch(rf0, fb);
-      if (ADV == DFX_ADV_TOKEN) l2_prefetch(ad0, fb);
       const uintptr_t m0 = reinterpret_cast<uintptr_t>(mk0) & ~uintptr_t(15);
       l2_prefetch(reinterpret_cast<const void*>(m0),
                   (uint32_t)((reinterpret_cast<uintptr_t>(mk0) + 4u * (uint32_t)nvec - m0 + 15u) & ~uintptr_t(15)));
