@@ -170,6 +170,7 @@ struct LossParams {
 // also owns the ids up to the source's slot count)
 __global__ void __launch_bounds__(256) slot_table_kernel(SlotGeom g, int64_t n_slots, const double* __restrict__ adv,
                                                          SlotEnt* __restrict__ tab) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the loss kernel may launch now (it waits)
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= g.n_seq) return;
   const int64_t a = __ldg(g.cu + s), b = __ldg(g.cu + s + 1);
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(256) slot_table_group_kernel(SlotGeom g, int64
                                                                const double* __restrict__ reward, double eps,
                                                                double* __restrict__ adv_out, int32_t* flags,
                                                                SlotEnt* __restrict__ tab) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n_records) return;
@@ -447,6 +449,10 @@ __device__ __forceinline__ void whiten_coeffs(const LossParams& p, double& mu, d
 // f64 across rounds), one deterministic warp reduction per slot.
 template <int ADV, int KL, bool DLOGP, int UNROLL = 2, int MINB = 3, bool MULTI = false>
 __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
+  // programmatic dependent launch: this grid starts while the slot-table pre-pass drains and waits here for it;
+  // the finalize kernel is released at once (it waits for this grid's completion)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -676,6 +682,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ], double* sh) {
 
 template <bool COUNTS>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinParams f) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent of the loss kernel)
   __shared__ double sh[(kFinThreads / 32) * 6];
   __shared__ bool is_last;
   const int gi = blockIdx.y;
@@ -851,6 +858,22 @@ SlotGeom geom_of(const dfx_packed* b, int64_t base, int64_t span) {
 }
 
 // persistent grid: as many 256-thread CTAs as fit on all SMs at once
+// launch as a programmatic dependent of the previous kernel in the stream (its launch and prologue overlap that
+// kernel's tail; the kernel itself waits with griddepcontrol.wait before reading what the previous one wrote)
+template <typename K, typename P>
+void pdl_launch(K kernel, dim3 grid, dim3 block, cudaStream_t st, const P& arg) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, arg);
+}
+
 template <int ADV, int KL, bool DL, int U, int MB>
 void launch_variant(const LossParams& p, cudaStream_t st) {
   static thread_local int cached_dev = -1, cached_blocks = 0;
@@ -864,8 +887,8 @@ void launch_variant(const LossParams& p, cudaStream_t st) {
     cached_dev = dev;
   }
   // a single source keeps the source index a compile-time 0 (no dynamic parameter indexing)
-  if (p.n_src > 1) loss_slots_kernel<ADV, KL, DL, U, MB, true><<<cached_blocks, 256, 0, st>>>(p);
-  else loss_slots_kernel<ADV, KL, DL, U, MB, false><<<cached_blocks, 256, 0, st>>>(p);
+  if (p.n_src > 1) pdl_launch(loss_slots_kernel<ADV, KL, DL, U, MB, true>, dim3(cached_blocks), dim3(256), st, p);
+  else pdl_launch(loss_slots_kernel<ADV, KL, DL, U, MB, false>, dim3(cached_blocks), dim3(256), st, p);
 }
 
 // Tuning knob (benchmarking only): DFX_LOSS_VARIANT=u2b3 (default) | u3b2 | u4b2 | u2b2 selects the
@@ -1122,7 +1145,7 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
   if (args->ev_main_end) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_end), stream));
   f.part = w.part;
   f.ticket = w.ticket;
-  finalize_kernel<false><<<fgrid, kFinThreads, 0, stream>>>(f);
+  pdl_launch(finalize_kernel<false>, fgrid, dim3(kFinThreads), stream, f);
   DFX_LAUNCH_CHECK("finalize_kernel");
   return DFX_OK;
 }
