@@ -92,6 +92,44 @@ static void test_advantage() {
         "KAT [1,0,1,0] eps 0 -> [1,-1,1,-1]");
 }
 
+// gpu_generate (device draw_tokens + hash_bytes) == fn_generate, payload bytes included; same errors
+static void test_generate() {
+  for (int kind = 0; kind < 2; ++kind) {
+    StageContext ctx;
+    ctx.run_seed = 17;
+    ctx.gen.rollouts_per_prompt = 5;
+    ctx.gen.response_tokens.kind = kind ? TokenDist::Kind::UNIFORM : TokenDist::Kind::CONSTANT;
+    ctx.gen.response_tokens.value = 37;
+    ctx.gen.response_tokens.min = 1;
+    ctx.gen.response_tokens.max = 300;
+    ctx.gen.bytes_per_token = 3;
+    SampleBatch a, b;
+    for (uint32_t i = 0; i < 64; ++i) {
+      SampleRecord r;
+      r.sample_id = 77 + 13 * i;
+      a.records.push_back(r);
+    }
+    b = a;
+    fn_generate(compute_node(), a, ctx);
+    dfx_distflow::gpu_generate(compute_node(), b, ctx);
+    CHECK(serialize_batch(a) == serialize_batch(b), kind ? "gpu_generate (UNIFORM) bit-exact vs fn_generate"
+                                                          : "gpu_generate (CONSTANT) bit-exact vs fn_generate");
+  }
+  StageContext bad;
+  bad.gen.response_tokens.kind = TokenDist::Kind::UNIFORM;
+  bad.gen.response_tokens.min = 9;
+  bad.gen.response_tokens.max = 8;
+  SampleBatch one;
+  one.records.push_back(SampleRecord{});
+  bool threw = false;
+  try {
+    dfx_distflow::gpu_generate(compute_node(), one, bad);
+  } catch (const Error&) {
+    threw = true;
+  }
+  CHECK(threw, "gpu_generate: max < min throws like fn_generate");
+}
+
 static void test_errors() {
   StageContext ctx;
   SampleBatch empty;
@@ -467,6 +505,7 @@ int main() {
     return 0;
   }
   test_advantage();
+  test_generate();
   test_errors();
   test_chain();
   test_loss();

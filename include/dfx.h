@@ -249,6 +249,21 @@ dfx_status dfx_synth_tokens(uint64_t seed, const uint64_t* ids, int64_t n_record
                             float* old_lp, float* ref_lp, float* value_tok, float* token_reward,
                             uint8_t* mask, int32_t* token_id, dfx_stream stream);
 
+/* fn_generate (distflow/functions.hpp:108-123) on the device, bit-exact.
+ * dfx_generate_counts: tok_count[s] (device u32, s = r * n_roll + j) =
+ *   draw_tokens(dist, seed, ids[r], j) (functions.hpp:67-80; kind 0 CONSTANT
+ *   (value), 1 UNIFORM [min, max], 2 SKEWED [min, max]). Errors as the
+ *   reference: rollouts_per_prompt < 1, max < min -> DFX_INVALID_ARGUMENT.
+ * dfx_generate_payload: payload bytes [payload_off[s], payload_off[s+1]) =
+ *   hash_bytes(keyed_hash(seed, "payload", ids[r], j), len) (hash.hpp:48-59);
+ *   payload_off: device i64 [n_records*n_roll + 1], the exclusive prefix of
+ *   tok_count * bytes_per_token. ids: device. */
+dfx_status dfx_generate_counts(uint64_t seed, int32_t kind, uint32_t value, uint32_t min_tokens, uint32_t max_tokens,
+                               const uint64_t* ids, int64_t n_records, int32_t n_roll, uint32_t* tok_count,
+                               dfx_stream stream);
+dfx_status dfx_generate_payload(uint64_t seed, const uint64_t* ids, int64_t n_records, int32_t n_roll,
+                                const int64_t* payload_off, uint8_t* payload, dfx_stream stream);
+
 /* ---------------------------------------------------------------------------
  * DataBuffer reshard (DP m->n), replacing BufferStore::exchange/get
  * (distflow/data_plane.hpp:237-442) and all_to_all (distflow/transport.hpp:718-754)

@@ -270,6 +270,55 @@ inline dfx_loss_out& last_loss() {
 }
 
 // ---- stage functions (exact StageFn signature, functions.hpp:63) ------------------------------------------------
+// fn_generate (functions.hpp:108-123) on the GPU: token counts (draw_tokens) and hash_bytes payloads computed by
+// dfx_generate_counts / dfx_generate_payload, bit-identical, then handed to the host records (the reference's
+// SampleBatch owns its payload bytes). Same errors: rollouts_per_prompt < 1, max < min.
+inline void gpu_generate(const distflow::NodeSpec& node, distflow::SampleBatch& batch, distflow::StageContext& ctx) {
+  (void)node;
+  if (ctx.gen.rollouts_per_prompt < 1) throw distflow::Error("rollouts_per_prompt must be >= 1");
+  const auto& td = ctx.gen.response_tokens;
+  const bool uni = td.kind == distflow::TokenDist::Kind::UNIFORM;
+  if (uni && td.max < td.min) throw distflow::Error("token distribution max < min");
+  Arena& ar = worker_arena();
+  const int64_t R = int64_t(batch.records.size()), n_roll = ctx.gen.rollouts_per_prompt, S = R * n_roll;
+  if (R == 0) return;
+  auto* hid = static_cast<uint64_t*>(ar.pinned("gen:ids", size_t(R) * 8));
+  for (int64_t r = 0; r < R; ++r) hid[r] = batch.records[size_t(r)].sample_id;
+  auto* did = static_cast<uint64_t*>(ar.device("gen:ids", size_t(R) * 8));
+  auto* dcnt = static_cast<uint32_t*>(ar.device("gen:counts", size_t(S) * 4));
+  auto* hcnt = static_cast<uint32_t*>(ar.pinned("gen:counts", size_t(S) * 4));
+  cuda_check(cudaMemcpyAsync(did, hid, size_t(R) * 8, cudaMemcpyHostToDevice, ar.stream), "H2D");
+  check(dfx_generate_counts(ctx.run_seed, uni ? 1 : 0, td.value, td.min, td.max, did, R, int32_t(n_roll), dcnt,
+                            ar.stream));
+  cuda_check(cudaMemcpyAsync(hcnt, dcnt, size_t(S) * 4, cudaMemcpyDeviceToHost, ar.stream), "D2H");
+  cuda_check(cudaStreamSynchronize(ar.stream), "sync");
+  auto* hoff = static_cast<int64_t*>(ar.pinned("gen:off", size_t(S + 1) * 8));
+  hoff[0] = 0;
+  for (int64_t s = 0; s < S; ++s) hoff[s + 1] = hoff[s] + int64_t(hcnt[s]) * ctx.gen.bytes_per_token;
+  const size_t total = size_t(hoff[S]);
+  auto* hpl = static_cast<uint8_t*>(ar.pinned("gen:payload", total + 1));
+  if (total) {
+    auto* doff = static_cast<int64_t*>(ar.device("gen:off", size_t(S + 1) * 8));
+    auto* dpl = static_cast<uint8_t*>(ar.device("gen:payload", total));
+    cuda_check(cudaMemcpyAsync(doff, hoff, size_t(S + 1) * 8, cudaMemcpyHostToDevice, ar.stream), "H2D");
+    check(dfx_generate_payload(ctx.run_seed, did, R, int32_t(n_roll), doff, dpl, ar.stream));
+    cuda_check(cudaMemcpyAsync(hpl, dpl, total, cudaMemcpyDeviceToHost, ar.stream), "D2H");
+    cuda_check(cudaStreamSynchronize(ar.stream), "sync");
+  }
+  int64_t s = 0;
+  for (auto& rec : batch.records) {
+    rec.rollouts.clear();
+    rec.rollouts.reserve(size_t(n_roll));
+    for (int64_t r = 0; r < n_roll; ++r, ++s) {
+      distflow::Rollout ro;
+      ro.token_count = hcnt[s];
+      ro.payload.assign(hpl + hoff[s], hpl + hoff[s + 1]);
+      rec.rollouts.push_back(std::move(ro));
+    }
+  }
+}
+
+
 // fn_group_advantage (functions.hpp:143-161) on the GPU: bit-identical f64 channel "advantage".
 inline void gpu_group_advantage(const distflow::NodeSpec& node, distflow::SampleBatch& batch,
                                 distflow::StageContext& ctx) {
@@ -332,7 +381,7 @@ inline void gpu_train(const distflow::NodeSpec& node, distflow::SampleBatch& bat
 // stand-ins upstream of the hot path stay the reference's own CPU functions.
 inline distflow::FunctionRegistry gpu_registry() {
   distflow::FunctionRegistry reg;
-  reg.register_fn("actor_generate", distflow::fn_generate);
+  reg.register_fn("actor_generate", gpu_generate);
   reg.register_fn("ref_logprob", distflow::fn_ref_logprob);
   reg.register_fn("value_inference", distflow::fn_value);
   reg.register_fn("reward_compute", distflow::fn_reward);
@@ -340,7 +389,7 @@ inline distflow::FunctionRegistry gpu_registry() {
   reg.register_fn("ppo_advantage", gpu_ppo_advantage);
   reg.register_fn("train_actor", gpu_train);
   reg.register_fn("train_critic", gpu_train);
-  reg.register_fn("ACTOR/MODEL_INFERENCE", distflow::fn_generate);
+  reg.register_fn("ACTOR/MODEL_INFERENCE", gpu_generate);
   reg.register_fn("REFERENCE/MODEL_INFERENCE", distflow::fn_ref_logprob);
   reg.register_fn("CRITIC/MODEL_INFERENCE", distflow::fn_value);
   reg.register_fn("REWARD/COMPUTE", distflow::fn_reward);

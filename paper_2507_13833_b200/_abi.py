@@ -85,6 +85,8 @@ def _declare(L):
     L.dfx_loss_combine.argtypes = [P, i32, i32, C.POINTER(LossCfg), P, P]
     L.dfx_check_flags.argtypes = [P, P]
     L.dfx_synth_tokens.argtypes = [u64, P, i64, i32, P, i64, i64, P, P, P, P, P, P, P, P]
+    L.dfx_generate_counts.argtypes = [u64, i32, C.c_uint32, C.c_uint32, C.c_uint32, P, i64, i32, P, P]
+    L.dfx_generate_payload.argtypes = [u64, P, i64, i32, P, P, P]
     L.dfx_event_create.argtypes = [C.POINTER(P)]
     L.dfx_event_destroy.argtypes = [P]
     L.dfx_event_record.argtypes = [P, P]
@@ -94,7 +96,8 @@ def _declare(L):
     for name in ("dfx_grpo_advantage", "dfx_broadcast_advantage", "dfx_ppo_advantage", "dfx_gae", "dfx_ppo_loss",
                  "dfx_gae_ppo_loss",
                  "dfx_ppo_loss_multi",
-                 "dfx_check_flags", "dfx_synth_tokens", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
+                 "dfx_check_flags", "dfx_synth_tokens", "dfx_generate_counts", "dfx_generate_payload",
+                 "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
                  "dfx_event_elapsed_ms"):
         getattr(L, name).restype = i32
 
@@ -103,7 +106,8 @@ def _declare(L):
 EXPORTS = ("dfx_last_error", "dfx_version", "dfx_grpo_advantage", "dfx_broadcast_advantage", "dfx_ppo_advantage",
            "dfx_gae_workspace_bytes", "dfx_gae", "dfx_ppo_loss_workspace_bytes", "dfx_ppo_loss",
            "dfx_ppo_loss_multi_workspace_bytes", "dfx_ppo_loss_multi", "dfx_check_flags",
-           "dfx_synth_tokens", "dfx_serialize_plan", "dfx_serialize_records",
+           "dfx_synth_tokens", "dfx_generate_counts", "dfx_generate_payload", "dfx_serialize_plan",
+           "dfx_serialize_records",
            "dfx_blob_index", "dfx_blob_unpack", "dfx_reward_stats", "dfx_loss_combine", "dfx_copy_batch",
            "dfx_copy_sm", "dfx_view_meta", "dfx_copy_many", "dfx_event_create", "dfx_event_destroy",
            "dfx_event_record", "dfx_event_elapsed_ms")

@@ -104,3 +104,36 @@ def rollout_channels(seed: int, ids, n_roll: int):
     reward = unit_from_hash(hash_combine(hash_combine(hash_str(seed, "reward"), rid), rr))
     value = symmetric_from_hash(hash_combine(hash_combine(hash_str(seed, "value"), rid), rr))
     return reward, value
+
+
+def generate_rollouts(seed: int, ids, n_roll: int, dist: TokenDist, bytes_per_token: int, stream=None):
+    """fn_generate (functions.hpp:108-123) on the device: per-rollout token counts (draw_tokens) and the
+    concatenated hash_bytes payloads (hash.hpp:48-59), bit-identical to the reference.
+    ids: device uint64/int64 tensor [R]. Returns (tok_count u32 [R*n_roll], payload_off i64 [R*n_roll+1],
+    payload u8 [total]) on the device. One host synchronisation (the payload size)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _abi
+
+    if n_roll < 1:
+        raise ValueError("rollouts_per_prompt must be >= 1")  # functions.hpp:111
+    L = _abi.lib()
+    R = int(ids.numel())
+    S = R * n_roll
+    dev = ids.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    kind = TokenDist.KINDS.index(dist.kind)
+    counts = torch.empty(max(S, 1), dtype=torch.int32, device=dev)
+    _abi.check(L.dfx_generate_counts(seed, kind, dist.value, dist.min, dist.max, C.c_void_p(ids.data_ptr()), R,
+                                     n_roll, C.c_void_p(counts.data_ptr()), C.c_void_p(s)))
+    off = torch.zeros(S + 1, dtype=torch.int64, device=dev)
+    if S:
+        torch.cumsum(counts[:S].to(torch.int64) * bytes_per_token, 0, out=off[1:])
+    total = int(off[-1].item())
+    payload = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+    if total:
+        _abi.check(L.dfx_generate_payload(seed, C.c_void_p(ids.data_ptr()), R, n_roll, C.c_void_p(off.data_ptr()),
+                                          C.c_void_p(payload.data_ptr()), C.c_void_p(s)))
+    return counts[:S].view(torch.uint32) if hasattr(torch, "uint32") else counts[:S], off, payload[:total]
