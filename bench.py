@@ -72,7 +72,7 @@ def parse():
                     help="c4: the native distributed DataBuffer (libdfx, one C call per verb, NCCL) or the Python "
                          "DeviceBufferStore")
     ap.add_argument("--transport", default="pull", choices=["pull", "nccl"],
-                    help="c4 native store: CUDA-IPC pulls by the copy engines (default) or NCCL send/recv")
+                    help="c4 native store: SM pulls of peer-mapped (CUDA IPC) producer memory (default) or NCCL send/recv")
     ap.add_argument("--placement", default="box", choices=["box", "store"],
                     help="box: one DataBuffer per box, 8 logical workers (SURVEY §8(e)); store: one DataBuffer per "
                          "GPU, 2 logical workers per GPU -> dense all-to-all at every N > 1")

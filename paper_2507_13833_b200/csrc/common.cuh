@@ -51,6 +51,22 @@ __device__ __forceinline__ uint32_t ldg_stream_u32(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
+// predicated forms: no load when pred is false (the outputs are then undefined and must not be used) -- a
+// predicated instruction instead of a branch around the asm, which the compiler cannot if-convert
+__device__ __forceinline__ float4 ldg_stream_f4_if(const float* p, bool pred) {
+  float4 r;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "r"((int)pred));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u32_if(const void* p, bool pred) {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.u32 %0, [%1];\n\t}"
+               : "=r"(r)
+               : "l"(p), "r"((int)pred));
+  return r;
+}
 __device__ __forceinline__ void stg_stream_f4(float* p, float4 v) {
   asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)
