@@ -143,6 +143,13 @@ __device__ __forceinline__ float k3_series(float x) {
   return (x * x) * q;
 }
 constexpr float kK3Series = 0.125f;
+// 2^x by MUFU.EX2 alone (flush-to-zero): exp2f's extra range reduction only matters below 2^-126, where the ratio
+// (and every term it enters) is zero for the loss anyway; identical bits elsewhere
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Exact clip decision s*(l - o) > s*T for f32 inputs l, o (d = f32(l - o)) against a threshold given as the float

@@ -256,7 +256,7 @@ __device__ __forceinline__ void gae_tile_loss(const GaeParams& p, int64_t T0, ui
         const float m = on ? 1.0f : 0.0f;
         const float l = f4_get(l4[u], k), o = f4_get(o4[u], k), rf = f4_get(f4[u], k), A = f4_get(a4, k);
         const float d = l - o;
-        const float rho = exp2f(d * kLog2e);
+        const float rho = ex2_ftz(d * kLog2e);
         const float rc = fminf(fmaxf(rho, p.lo1), p.hi1);
         lpg = fmaf(m, fmaxf(-A * rho, -A * rc), lpg);
         const float sg = A < 0.0f ? -1.0f : 1.0f;

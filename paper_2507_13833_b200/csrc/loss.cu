@@ -323,7 +323,7 @@ __device__ __forceinline__ void loss_vec(const LossParams& p, const UnitAdv& ua,
     if (!FULL) on = on && (t + k >= t0) && (t + k < t1);
     const float m = on ? 1.0f : 0.0f;
     const float d = dd[k];
-    const float rho = exp2f(d * kLog2e);     // MUFU.EX2, ~2 ulp
+    const float rho = ex2_ftz(d * kLog2e);   // MUFU.EX2, ~2 ulp
     float A, pg;
     if constexpr (ADV == DFX_ADV_TOKEN) {
       A = At[k];
