@@ -524,6 +524,9 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     uint32_t nclip = 0u, nmask = 0u;
     const int64_t vbeg = t0 >> 2;
     const int32_t nvec = (int32_t)(((t1 + 3) >> 2) - vbeg);
+    // vectors [i_lo, i_lo + n_full) hold four tokens of the slot each
+    const int32_t i_lo = (int32_t)(((t0 + 3) >> 2) - vbeg);
+    const uint32_t n_full = (uint32_t)max((int64_t)0, (t1 >> 2) - vbeg - i_lo);
     const float* lp0 = S.lp + 4 * vbeg;
     const float* ol0 = S.old_lp + 4 * vbeg;
     const float* rf0 = S.ref_lp + 4 * vbeg;
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         if (i >= nvec) break;
         const int64_t t = 4 * (vbeg + i);
         float aout[4], gout[4];
-        if (t >= t0 && t + 4 <= t1) {
+        if ((uint32_t)(i - i_lo) < n_full) {  // all four tokens inside the slot (32-bit test)
           loss_vec<ADV, KL, DLOGP, true>(p, ua, lv[j], ov[j], rv[j], av[j], mk[j], t, t0, t1, wf, w, acc, aout,
                                          gout);
           if (atout) store_vec<true>(atout, t, t0, t1, aout);
