@@ -67,6 +67,9 @@ __device__ __forceinline__ uint32_t ldg_stream_u32_if(const void* p, bool pred) 
                : "l"(p), "r"((int)pred));
   return r;
 }
+__device__ __forceinline__ void prefetch_l2_if(const void* p, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q prefetch.global.L2 [%0];\n\t}" ::"l"(p), "r"((int)pred));
+}
 __device__ __forceinline__ void stg_stream_f4(float* p, float4 v) {
   asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)

@@ -18,6 +18,9 @@
 #ifndef DFX_LOSS_PRED
 #define DFX_LOSS_PRED 1  // predicated stream loads instead of a branch per vector (C2 step -1.8%)
 #endif
+#ifndef DFX_LOSS_PFR
+#define DFX_LOSS_PFR 1  // per-lane L2 prefetch of the vectors this many rounds ahead (1: C2 step -3%; 2, 3: slower)
+#endif
 #ifndef DFX_LOSS_PF
 // (kernel-variant sweeps) L2 bulk prefetch of each claimed slot's streams. Measured at C2: the loss launch drops
 // from 0.1065 to 0.1034 ms, but the step only by 0.5%: the prefetches still in flight when the kernel retires slow
@@ -561,6 +564,16 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         rv[j] = ldg_stream_f4_if(rf0 + 4 * i, in);
         mk[j] = ldg_stream_u32_if(mk0 + 4 * i, in);
         if (ADV == DFX_ADV_TOKEN) av[j] = ldg_stream_f4_if(ad0 + 4 * i, in);
+#if DFX_LOSS_PFR
+        {  // the next round's vectors of this lane into L2 (no registers held)
+          const int32_t i2 = i + 32 * kUnroll * DFX_LOSS_PFR;
+          const bool in2 = i2 < nvec;
+          prefetch_l2_if(lp0 + 4 * i2, in2);
+          prefetch_l2_if(ol0 + 4 * i2, in2);
+          prefetch_l2_if(rf0 + 4 * i2, in2);
+          if ((lane & 7) == 0) prefetch_l2_if(mk0 + 4 * i2, in2);  // (one 128-byte line per 8 lanes)
+        }
+#endif
 #else
         if (i < nvec) {
           lv[j] = ldg_stream_f4(lp0 + 4 * i);
