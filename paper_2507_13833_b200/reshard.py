@@ -301,7 +301,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     tmpl = templates.get(template_key) if (templates is not None and pull and not lazy) else None
     if tmpl is not None:
         tmpl["hits"] = tmpl.get("hits", 0) + 1
-        return _exchange_from_template(tmpl, L, dev, st, group)
+        return _exchange_from_template(tmpl, L, dev, st, group, plan)
 
     # 1. per-segment table filled by the owner: rollouts, tokens, first token mod 16 (NCCL alignment),
     #    and (pull) the absolute token / rollout / record offsets in the owner's arrays
@@ -340,19 +340,19 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
             r_a, r_b = loc[order[0]][1], loc[order[-1]][2]
             view = b0 if (r_a == 0 and r_b == b0.n_records) else b0.view_records(r_a, r_b)
             if pull:  # peers may pull from us: take part in both barriers
-                _device_barrier(group, dev)
+                _sync_if(plan, group, dev)
                 sent = sum(int(sizes[i, 1]) for i, (d, p, *_r) in enumerate(plan.segs) if i in loc
                            for r in plan.dst_ranks[d] if r != rank)
                 if lazy:  # the closing barrier is issued at release(), in step with the lazy consumers'
                     return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0,
-                                         release=lambda: _device_barrier(group, dev))
-                _device_barrier(group, dev)
+                                         release=lambda: _sync_if(plan, group, dev))
+                _sync_if(plan, group, dev)
                 return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, 0)
             _, sent, recv_b, _ = _p2p(plan, loc, sizes, dev, st, group, ch_names, None)
             return ConsumerBatch(view, groups, rec_off, roll_off, True, sent, recv_b)
 
     if lazy and pull:
-        _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+        _sync_if(plan, group, dev)  # every producer's stream has passed its production of these batches
         per_group = []
         for d in groups:
             srcs = []
@@ -374,7 +374,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
         recv_b = sum(int(sizes[i, 1]) * sum(torch.empty(0, dtype=dt_).element_size() for dt_ in stream_specs.values())
                      for i in order if i not in loc)
         return ConsumerBatch(None, groups, rec_off, roll_off, False, 0, recv_b, per_group,
-                             release=lambda: _device_barrier(group, dev), ipc_bases=opened)
+                             release=lambda: _sync_if(plan, group, dev), ipc_bases=opened)
 
     # 3. allocate the consumer batch
     R, S, T = rec_off[-1], roll_off[-1], tok_off[-1]
@@ -396,7 +396,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     sent = recv_b = 0
     recvd = []
     if pull:
-        _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+        _sync_if(plan, group, dev)  # every producer's stream has passed its production of these batches
         for i in order:
             if i in loc:
                 continue
@@ -448,7 +448,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
                                         C.cast(chp, C.c_void_p), st.cuda_stream))
         out._keep = [recvd]
     if pull:
-        _device_barrier(group, dev)  # peers may reuse their buffers once every consumer has pulled
+        _sync_if(plan, group, dev)  # peers may reuse their buffers once every consumer has pulled
     t_ = _mark("unpack", t_)
     # host offsets of the consumer batch are fetched lazily (PackedBatch.ensure_host_meta): no D2H here
     out.host_group_off, out.host_cu = None, None
@@ -482,7 +482,7 @@ def exchange(plan: Plan, sources: dict, stream=None, group=None, schema=None, me
     return cbatch
 
 
-def _exchange_from_template(tm: dict, L, dev, st, group) -> ConsumerBatch:
+def _exchange_from_template(tm: dict, L, dev, st, group, plan) -> ConsumerBatch:
     """A materialized pull whose producers are exactly those of the template (same memory, extents and
     placement on every rank): fresh consumer buffers, the recorded copies in one call, one unpack."""
     out = _alloc_batch(tm["R"], tm["S"], tm["T"], tm["ch"], tm["specs"], dev)
@@ -491,25 +491,25 @@ def _exchange_from_template(tm: dict, L, dev, st, group) -> ConsumerBatch:
     dsts = np.array([base[k] + off for k, off, _, _ in cp], np.uint64)
     srcs = np.array([a for _, _, a, _ in cp], np.uint64)
     nbs = np.array([n for _, _, _, n in cp], np.uint64)
-    _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+    _sync_if(plan, group, dev)  # every producer's stream has passed its production of these batches
     _abi.check(L.dfx_copy_many(len(cp), dsts.ctypes.data, srcs.ctypes.data, nbs.ctypes.data, st.cuda_stream))
     if tm["n_metas"]:
         chp = (C.c_void_p * max(1, len(tm["ch"])))(*[out.channels[c].data_ptr() for c in tm["ch"]])
         _abi.check(L.dfx_reshard_unpack(C.cast(tm["metas"], C.c_void_p), tm["n_metas"], len(tm["ch"]),
                                         out.ids.data_ptr(), out.group_off.data_ptr(), out.roll_group.data_ptr(),
                                         out.cu_seqlens.data_ptr(), C.cast(chp, C.c_void_p), st.cuda_stream))
-    _device_barrier(group, dev)  # peers may reuse their buffers once every consumer has pulled
+    _sync_if(plan, group, dev)  # peers may reuse their buffers once every consumer has pulled
     out.host_group_off, out.host_cu = tm["h_go"], tm["h_cu"]
     return ConsumerBatch(out, tm["groups"], tm["rec_off"], tm["roll_off"], False, tm["sent"], tm["recv"])
 
 
-def reuse_lazy(prev: ConsumerBatch, group) -> ConsumerBatch:
+def reuse_lazy(prev: ConsumerBatch, group, plan) -> ConsumerBatch:
     """A lazy consumer batch for a step whose producer batches are the ones `prev` mapped (same memory and
     extents on every rank, checked by the store): same sources, fresh ordering barriers."""
     dev = torch.device("cuda", torch.cuda.current_device())
-    _device_barrier(group, dev)  # every producer's stream has passed its production of these batches
+    _sync_if(plan, group, dev)  # every producer's stream has passed its production of these batches
     return ConsumerBatch(None, prev.groups, prev.rec_off, prev.roll_off, False, prev.bytes_sent, prev.bytes_recv,
-                         prev.sources, release=lambda: _device_barrier(group, dev))
+                         prev.sources, release=lambda: _sync_if(plan, group, dev))
 
 
 def reuse_zero_copy(prev: ConsumerBatch, plan: Plan, sources: dict, group) -> ConsumerBatch:
@@ -524,12 +524,20 @@ def reuse_zero_copy(prev: ConsumerBatch, plan: Plan, sources: dict, group) -> Co
     if not _distributed(group):
         return ConsumerBatch(view, prev.groups, prev.rec_off, prev.roll_off, True, 0, 0)
     dev = view.device
-    _device_barrier(group, dev)
+    _sync_if(plan, group, dev)
     return ConsumerBatch(view, prev.groups, prev.rec_off, prev.roll_off, True, prev.bytes_sent, 0,
-                         release=lambda: _device_barrier(group, dev))
+                         release=lambda: _sync_if(plan, group, dev))
 
 
 _BARRIER = {}
+
+
+def _sync_if(plan, group, dev):
+    """The exchange's ordering barrier, needed only when some record crosses GPUs: with every consumer group on the
+    GPU of its producer groups (box placements on <= 4 GPUs) no rank reads another's memory, stream order alone
+    orders production before consumption, and every rank skips it alike (plan.cross is global)."""
+    if plan.cross:
+        _device_barrier(group, dev)
 
 
 def _device_barrier(group, dev):

@@ -128,7 +128,7 @@ class DeviceBufferStore:
             # all ranks take this branch together and issue the same collectives
             prev = tmpl[1]
             e.ready = (reuse_zero_copy(prev, plan, sources, self.group) if prev.sources is None
-                       else reuse_lazy(prev, self.group))
+                       else reuse_lazy(prev, self.group, plan))
             self.template_hits += 1
         else:
             e.ready = exchange(plan, sources, stream=self.stream, group=self.group, schema=self.schema,
