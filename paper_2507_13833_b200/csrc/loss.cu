@@ -139,6 +139,7 @@ struct SlotEnt {
 
 struct LossParams {
   int n_src;
+  int multi;  // sources from dfx_ppo_loss_multi (may be peer-mapped memory): the MULTI kernel, even for one source
   LossSrc src[kMaxLossSrc];
   int64_t n_slots;
   int64_t n_records;
@@ -565,7 +566,10 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         mk[j] = ldg_stream_u32_if(mk0 + 4 * i, in);
         if (ADV == DFX_ADV_TOKEN) av[j] = ldg_stream_f4_if(ad0 + 4 * i, in);
 #if DFX_LOSS_PFR
-        {  // the next round's vectors of this lane into L2 (no registers held)
+        // the next round's vectors of this lane into L2 (no registers held). Single-source kernel only: its batch
+        // is in this GPU's memory (dfx_ppo_loss); prefetch.global.L2 of NVLink-mapped memory (the multi-source
+        // kernel's partner sources) stalls the kernel ~50x
+        if constexpr (!MULTI) {
           const int32_t i2 = i + 32 * kUnroll * DFX_LOSS_PFR;
           const bool in2 = i2 < nvec;
           prefetch_l2_if(lp0 + 4 * i2, in2);
@@ -915,7 +919,7 @@ void launch_variant(const LossParams& p, cudaStream_t st) {
     cached_dev = dev;
   }
   // a single source keeps the source index a compile-time 0 (no dynamic parameter indexing)
-  if (p.n_src > 1) pdl_launch(loss_slots_kernel<ADV, KL, DL, U, MB, true>, dim3(cached_blocks), dim3(256), st, p);
+  if (p.n_src > 1 || p.multi) pdl_launch(loss_slots_kernel<ADV, KL, DL, U, MB, true>, dim3(cached_blocks), dim3(256), st, p);
   else pdl_launch(loss_slots_kernel<ADV, KL, DL, U, MB, false>, dim3(cached_blocks), dim3(256), st, p);
 }
 
@@ -935,7 +939,7 @@ template <int ADV, int KL, bool DL>
 void launch_slots(const LossParams& p, cudaStream_t st) {
   // (the tuning variants are instantiated for the hot configuration only)
   if constexpr (ADV == DFX_ADV_ROLLOUT && KL == DFX_KL_K3 && !DL) {
-    if (p.n_src > 1) {
+    if (p.n_src > 1 || p.multi) {
       // sources read over NVLink have ~2x the latency of local HBM: more vectors in flight per lane
       static const int mu =
           std::getenv("DFX_LOSS_MULTI_UNROLL") ? std::atoi(std::getenv("DFX_LOSS_MULTI_UNROLL")) : 4;
@@ -1027,7 +1031,7 @@ size_t dfx_ppo_loss_multi_workspace_bytes(const dfx_loss_src* srcs, int32_t n_sr
 
 namespace {
 
-dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
+dfx_status ppo_loss_impl(bool multi_api, const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
                          const dfx_loss_args* args, void* workspace, size_t ws_bytes, cudaStream_t stream) {
   if (!srcs || n_src < 1 || !cfg || !args || !args->out) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss: null argument");
   if (n_src > kMaxLossSrc) return fail(DFX_INVALID_ARGUMENT, "dfx_ppo_loss_multi: at most 4 sources");
@@ -1117,6 +1121,7 @@ dfx_status ppo_loss_impl(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss
   const dfx_packed* b0 = &srcs[0].b;
   LossParams p{};
   p.n_src = n_src;
+  p.multi = multi_api ? 1 : 0;
   for (int32_t k = 0; k < n_src; ++k) p.src[k] = src[k];
   p.n_slots = n_slots;
   p.n_records = b0->n_records;
@@ -1193,12 +1198,12 @@ dfx_status dfx_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t token_s
   s.adv_tok_in = args->adv_tok_in;
   s.adv_tok_out = args->adv_tok_out;
   s.dlogp = args->dlogp;
-  return ppo_loss_impl(&s, 1, cfg, args, workspace, ws_bytes, stream);
+  return ppo_loss_impl(false, &s, 1, cfg, args, workspace, ws_bytes, stream);
 }
 
 dfx_status dfx_ppo_loss_multi(const dfx_loss_src* srcs, int32_t n_src, const dfx_loss_cfg* cfg,
                               const dfx_loss_args* args, void* workspace, size_t ws_bytes, dfx_stream stream) {
-  return ppo_loss_impl(srcs, n_src, cfg, args, workspace, ws_bytes, stream);
+  return ppo_loss_impl(true, srcs, n_src, cfg, args, workspace, ws_bytes, stream);
 }
 
 dfx_status dfx_loss_combine(const dfx_loss_out* parts, int32_t n_parts, int32_t n_groups, const dfx_loss_cfg* cfg,
