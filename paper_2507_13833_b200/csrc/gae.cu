@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   }
   // (programmatic dependent launch: everything above overlapped the prep kernel; the bitmap and epoch need it done)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the finish kernel waits for this grid
   // this thread's rollout-end bits (32 tokens = one aligned 32-bit word of the bitmap), cleared once read
   uint32_t last = 0u;
   if (c0 < rd_end) {
@@ -590,6 +591,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
     mbar_fence_init();
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the prep grid: bitmap, bounds, epoch, ticket reset
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the finish kernel waits for this grid
   unsigned long long* tr = p.trace ? p.trace + 32 * blockIdx.x : nullptr;
   int nseg_done = 0;
   if (tr && tid == 0) tr[0] = gtimer();
@@ -867,6 +869,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
 // ---- whitening sums: fixed-shape reduction of the per-tile partials ---------------------------------------------
 __global__ void __launch_bounds__(256) gae_finish_kernel(const double* __restrict__ part, int64_t n_tiles,
                                                          double* __restrict__ whiten) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent of the scan)
   __shared__ double s_red[8][3];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double tot[3] = {0.0, 0.0, 0.0};
@@ -891,6 +894,7 @@ __global__ void __launch_bounds__(256) gae_finish_kernel(const double* __restric
 __global__ void __launch_bounds__(256) gae_loss_finish_kernel(const double* __restrict__ lpart, int64_t n_tiles,
                                                               const uint8_t* __restrict__ seq_has, int64_t n_seq,
                                                               double beta, dfx_loss_out* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent of the scan)
   __shared__ double s_red[8][6];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double tot[6] = {0, 0, 0, 0, 0, 0};
@@ -969,6 +973,21 @@ inline int gae_variant(bool fused) {
     return s == "lb" ? 1 : s == "lb64" ? 2 : 0;
   }();
   return v >= 0 ? v : (fused ? 1 : 0);
+}
+
+// one 256-thread CTA as a programmatic dependent of the previous kernel (the finish kernels)
+template <typename... A>
+void gae_pdl_launch(void (*kernel)(A...), cudaStream_t st, A... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 template <typename K>
@@ -1135,7 +1154,8 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
   }
   DFX_LAUNCH_CHECK("gae scan");
   if (whiten) {
-    gae_finish_kernel<<<1, 256, 0, stream>>>(p.part, v == 0 ? p.n_segs : p.n_tiles, whiten);
+    gae_pdl_launch(gae_finish_kernel, stream, (const double*)p.part, (int64_t)(v == 0 ? p.n_segs : p.n_tiles),
+                   whiten);
     DFX_LAUNCH_CHECK("gae_finish_kernel");
   }
   return DFX_OK;
@@ -1208,8 +1228,8 @@ dfx_status dfx_gae_ppo_loss(const dfx_packed* b, int64_t token_base, int64_t tok
     default: gae_launch_seg<true>(p, stream); break;
   }
   DFX_LAUNCH_CHECK("gae scan<loss>");
-  gae_loss_finish_kernel<<<1, 256, 0, stream>>>(p.lpart, v == 0 ? p.n_segs : p.n_tiles, p.seq_has, p.n_seq,
-                                                 cfg->beta, out);
+  gae_pdl_launch(gae_loss_finish_kernel, stream, (const double*)p.lpart, (int64_t)(v == 0 ? p.n_segs : p.n_tiles),
+                 (const uint8_t*)p.seq_has, p.n_seq, cfg->beta, out);
   DFX_LAUNCH_CHECK("gae_loss_finish_kernel");
   return DFX_OK;
 }

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <string>
 
+#include <utility>
+
 #include "common.cuh"
 
 #ifndef DFX_CLIP_MODE
@@ -178,6 +180,7 @@ struct LossParams {
 __global__ void __launch_bounds__(256) slot_table_kernel(SlotGeom g, int64_t n_slots, const double* __restrict__ adv,
                                                          SlotEnt* __restrict__ tab) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the loss kernel may launch now (it waits)
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent: the advantages of the previous kernel)
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= g.n_seq) return;
   const int64_t a = __ldg(g.cu + s), b = __ldg(g.cu + s + 1);
@@ -385,6 +388,7 @@ __global__ void __launch_bounds__(256) slot_table_group_kernel(SlotGeom g, int64
                                                                double* __restrict__ adv_out, int32_t* flags,
                                                                SlotEnt* __restrict__ tab) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n_records) return;
@@ -892,8 +896,8 @@ SlotGeom geom_of(const dfx_packed* b, int64_t base, int64_t span) {
 // persistent grid: as many 256-thread CTAs as fit on all SMs at once
 // launch as a programmatic dependent of the previous kernel in the stream (its launch and prologue overlap that
 // kernel's tail; the kernel itself waits with griddepcontrol.wait before reading what the previous one wrote)
-template <typename K, typename P>
-void pdl_launch(K kernel, dim3 grid, dim3 block, cudaStream_t st, const P& arg) {
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -903,7 +907,7 @@ void pdl_launch(K kernel, dim3 grid, dim3 block, cudaStream_t st, const P& arg) 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, arg);
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 template <int ADV, int KL, bool DL, int U, int MB>
@@ -1156,16 +1160,16 @@ dfx_status ppo_loss_impl(bool multi_api, const dfx_loss_src* srcs, int32_t n_src
   p.ticket = w.slot_ticket;
   p.tab = w.tab;
   if (cfg->adv_source == DFX_ADV_GROUP_FUSED) {  // single source: the table pre-pass computes the advantages
-    slot_table_group_kernel<<<(unsigned)((b0->n_records + 7) / 8), 256, 0, stream>>>(
-        src[0].g, n_slots, b0->n_records, b0->group_off, b0->reward, cfg->adv_eps, p.adv_roll_out, args->flags, w.tab);
+    pdl_launch(slot_table_group_kernel, dim3((unsigned)((b0->n_records + 7) / 8)), dim3(256), stream, src[0].g, n_slots,
+               (int64_t)b0->n_records, b0->group_off, b0->reward, cfg->adv_eps, p.adv_roll_out, args->flags, w.tab);
     DFX_LAUNCH_CHECK("slot_table_group_kernel");
   }
   for (int32_t k = 0; k < n_src && cfg->adv_source != DFX_ADV_GROUP_FUSED; ++k) {  // the slot table of every source
     if (srcs[k].b.n_rollouts <= 0) continue;
     const int64_t nk = (k + 1 < n_src ? src[k + 1].slot0 : n_slots) - src[k].slot0;
     const double* adv = cfg->adv_source == DFX_ADV_ROLLOUT ? srcs[k].adv_roll : nullptr;
-    slot_table_kernel<<<(unsigned)((srcs[k].b.n_rollouts + 255) / 256), 256, 0, stream>>>(src[k].g, nk, adv,
-                                                                                        w.tab + src[k].slot0);
+    pdl_launch(slot_table_kernel, dim3((unsigned)((srcs[k].b.n_rollouts + 255) / 256)), dim3(256), stream, src[k].g,
+               nk, adv, w.tab + src[k].slot0);
     DFX_LAUNCH_CHECK("slot_table_kernel");
   }
   if (args->ev_main_begin) DFX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(args->ev_main_begin), stream));
