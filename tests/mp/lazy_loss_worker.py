@@ -88,6 +88,31 @@ for it, (dist_kind, hi) in enumerate((("uniform", 700), ("skewed", 3000), ("unif
     assert again.cpu().numpy().tobytes() == res["out"].cpu().numpy().tobytes()
     lazy_store.worker_done(it + 100)
     print(f"rank {rank} case {it}: loss {got[0]:.9f} == {want[0]:.9f}, {int(got[5])} tokens", flush=True)
+# performance guard: the multi-source loss reading the partner's group over NVLink must run at NVLink speed (a
+# per-lane L2 prefetch of peer-mapped memory once slowed it 50x while every numeric check above still passed)
+big = dfx.PackedBatch.synthetic(9, 256, 16, dfx.TokenDist("uniform", 0, 1, 4096), device=dev, first_id=rank * 256)
+ctx = dfx.StageContext()
+dfx.fn_group_advantage(dfx.NodeSpec("adv"), big, ctx)
+store = DeviceBufferStore(Topology.box(2, world), rank, {"s": StoreStagePlan(Layout(2, 1), Layout(1, 2))},
+                          meta_group=meta)
+store.put("s", 500, rank, 0, big)
+cb = store.ensure_ready("s", 500, Layout(1, 2), lazy=True)
+srcs = cb.sources[0]
+remote = [x for x in srcs if isinstance(x, RemoteSource)][0]
+run = lambda: dfx.ppo_loss_sources(srcs, ctx, loss_group_off=cb.roll_off, device=dev)  # noqa: E731
+run()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    run()
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+gbs = remote.token_span * 13 / (ms / 1e3) / 1e9  # lp, old, ref (f32) + mask (u8) of the partner's tokens
+print(f"rank {rank}: multi-source loss {ms:.3f} ms, partner tokens read at {gbs:.0f} GB/s over NVLink", flush=True)
+assert gbs > 100, f"multi-source NVLink loss too slow: {gbs:.1f} GB/s"
+store.worker_done(500)
 dist.barrier()
 print("LAZY_OK", flush=True)
 dist.destroy_process_group()
