@@ -352,17 +352,30 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   // (ident) and never stored.
   const int s0 = lane & 7;
   const float vn_cross = s_v[tid * 32 + 32];  // first V of the next thread (or the token after the tile)
+  const uint32_t mn_cross = s_m[tid * 32 + 32] ? 1u : 0u;
   double Hd = 0.0, Hc = 1.0, Td = 0.0, Tc = 1.0;  // the thread's 32-token map, f64
   uint32_t link = 0u, mbits = 0u;
+  // the successor (V, mask) of chunk ch is the first token of chunk ch + 1: from the next chunk in the rotated
+  // order, loaded one step ahead (scalar shared loads at the 128-byte thread stride are 32-way bank conflicts);
+  // chunk s's first V and mask are kept for the wrap-around and for pass 2
+  float4 r4n = *reinterpret_cast<const float4*>(s_r + tid * 32 + s0 * 4);
+  float4 v4n = *reinterpret_cast<const float4*>(s_v + tid * 32 + s0 * 4);
+  uint32_t m4n = *reinterpret_cast<const uint32_t*>(s_m + tid * 32 + s0 * 4);
+  const float v_s0first = v4n.x;
+  const uint32_t m_s0first = (m4n & 0xffu) ? 1u : 0u;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int ch = (s0 + j) & 7;
-    const int i0 = tid * 32 + ch * 4;
-    const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
-    const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
-    const uint32_t m4 = *reinterpret_cast<const uint32_t*>(s_m + i0);
-    const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
-    const uint32_t mnx = s_m[i0 + 4] ? 1u : 0u;
+    const float4 r4 = r4n, v4 = v4n;
+    const uint32_t m4 = m4n;
+    if (j < 7) {
+      const int chn = (s0 + j + 1) & 7;
+      r4n = *reinterpret_cast<const float4*>(s_r + tid * 32 + chn * 4);
+      v4n = *reinterpret_cast<const float4*>(s_v + tid * 32 + chn * 4);
+      m4n = *reinterpret_cast<const uint32_t*>(s_m + tid * 32 + chn * 4);
+    }
+    const float vnx = ch == 7 ? vn_cross : (j < 7 ? v4n.x : v_s0first);
+    const uint32_t mnx = ch == 7 ? mn_cross : (j < 7 ? ((m4n & 0xffu) ? 1u : 0u) : m_s0first);
     const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
     double fd = 0.0, fc = 1.0;
 #pragma unroll
@@ -421,8 +434,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
   const double Xin = fma(E.c, Xd, E.d);
   double X = fma(Tc, Xin, Td);
   float wa = 0.0f, wa2 = 0.0f;
-  float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
-  int pend_i = -1;
+  float vprev = v_s0first;  // the first V of the chunk processed before (chunk ch + 1); position 0: chunk s
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int ch = (s0 - 1 - j) & 7;
@@ -430,8 +442,8 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
     const int i0 = tid * 32 + ch * 4;
     const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
     const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
-    const float vnx = ch == 7 ? vn_cross : s_v[i0 + 4];
-    if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+    const float vnx = ch == 7 ? vn_cross : vprev;
+    vprev = v4.x;
     const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
     float oa[4], orr[4];
 #pragma unroll
@@ -451,9 +463,8 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
       }
     }
     if (interior || LOSS) *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
-    if (interior) {
-      pendR = make_float4(orr[0], orr[1], orr[2], orr[3]);
-      pend_i = i0;
+    if (interior) {  // (every successor value of this thread is in registers: R over V at once)
+      *reinterpret_cast<float4*>(s_v + i0) = make_float4(orr[0], orr[1], orr[2], orr[3]);
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -464,7 +475,6 @@ __global__ void __launch_bounds__(THREADS, MINB) gae_smem_kernel(GaeParams p) {
       }
     }
   }
-  if (interior) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
   if (interior || LOSS) {
     fence_proxy_async_smem();
     __syncthreads();
@@ -675,15 +685,24 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
       }
       // pass 1: chunk maps in the per-lane rotated order (conflict-free 128-bit shared reads); a chunk of four
       // linked tokens inside the segment (the common case) takes the select-free path
+      // The successor value of chunk ch (the first V of chunk ch + 1) comes from registers: the next chunk in the
+      // rotated order is loaded one step ahead (a scalar shared load at the 64-byte thread stride would be a 16-way
+      // bank conflict); chunk s's first V is kept for the wrap-around and for pass 2
       const float vn_cross = s_v[tid * kSegTPT + kSegTPT];
       double Hd = 0.0, Hc = 1.0, Td = 0.0, Tc = 1.0;
+      float4 r4n = *reinterpret_cast<const float4*>(s_r + tid * kSegTPT + s0 * 4);
+      float4 v4n = *reinterpret_cast<const float4*>(s_v + tid * kSegTPT + s0 * 4);
+      const float v_s0first = v4n.x;
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int ch = (s0 + jj) & 3;
-        const int i0 = tid * kSegTPT + ch * 4;
-        const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
-        const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
-        const float vnx = ch == 3 ? vn_cross : s_v[i0 + 4];
+        const float4 r4 = r4n, v4 = v4n;
+        if (jj < 3) {
+          const int chn = (s0 + jj + 1) & 3;
+          r4n = *reinterpret_cast<const float4*>(s_r + tid * kSegTPT + chn * 4);
+          v4n = *reinterpret_cast<const float4*>(s_v + tid * kSegTPT + chn * 4);
+        }
+        const float vnx = ch == 3 ? vn_cross : (jj < 3 ? v4n.x : v_s0first);
         const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
         const uint32_t l4 = (lkb >> (4 * ch)) & 0xfu, id4 = (ident >> (4 * ch)) & 0xfu;
         double fd = 0.0, fc = 1.0;
@@ -735,8 +754,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
       double X = fma(Tc, Xin, Td);
       float wa = 0.0f, wa2 = 0.0f;
       uint32_t wn = 0u;
-      float4 pendR = make_float4(0.f, 0.f, 0.f, 0.f);
-      int pend_i = -1;
+      float vprev = v_s0first;  // the first V of the chunk processed before (chunk ch + 1); position 0: chunk s
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int ch = (s0 - 1 - jj) & 3;
@@ -744,8 +762,8 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
         const int i0 = tid * kSegTPT + ch * 4;
         const float4 r4 = *reinterpret_cast<const float4*>(s_r + i0);
         const float4 v4 = *reinterpret_cast<const float4*>(s_v + i0);
-        const float vnx = ch == 3 ? vn_cross : s_v[i0 + 4];
-        if (interior && pend_i >= 0) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
+        const float vnx = ch == 3 ? vn_cross : vprev;
+        vprev = v4.x;
         const float rr[4] = {r4.x, r4.y, r4.z, r4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
         float oa[4], orr[4];
         const uint32_t l4 = (lkb >> (4 * ch)) & 0xfu, id4 = (ident >> (4 * ch)) & 0xfu;
@@ -782,9 +800,8 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
           wn += __popc((onm >> (4 * ch)) & 0xfu);
         }
         *reinterpret_cast<float4*>(s_r + i0) = make_float4(oa[0], oa[1], oa[2], oa[3]);
-        if (interior) {
-          pendR = make_float4(orr[0], orr[1], orr[2], orr[3]);
-          pend_i = i0;
+        if (interior) {  // (every successor value of this thread is in registers: R over V at once)
+          *reinterpret_cast<float4*>(s_v + i0) = make_float4(orr[0], orr[1], orr[2], orr[3]);
         } else {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
@@ -795,7 +812,6 @@ __global__ void __launch_bounds__(kSegThreads, 4) gae_seg_kernel(GaeParams p) {
           }
         }
       }
-      if (interior) *reinterpret_cast<float4*>(s_v + pend_i) = pendR;
       if (WHITEN) {
         wsum += (double)wa;
         wsq += (double)wa2;
