@@ -30,6 +30,49 @@ __global__ void a2a_kernel(Ptrs p, size_t n16) {
   for (; i < n16; i += step) dst[i] = src[i];
 }
 
+// TMA pull: each CTA streams its share of a pair's bytes through shared memory with bulk copies (peer global ->
+// shared, shared -> local global), 4 stages of 16 KB in flight
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(32) a2a_tma_kernel(Ptrs p, size_t bytes) {
+  constexpr int kStages = 4;
+  constexpr unsigned kChunk = 16384;
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long bar[kStages];
+  const int pr = blockIdx.x % p.n, cta_per = gridDim.x / p.n, b = blockIdx.x / p.n;
+  const unsigned char* src = reinterpret_cast<const unsigned char*>(p.src[pr]);
+  unsigned char* dst = reinterpret_cast<unsigned char*>(p.dst[pr]);
+  const size_t n_chunks = bytes / kChunk;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned phase = 0;
+    size_t issued = 0, done = 0;
+    const size_t mine = (n_chunks > (size_t)b) ? (n_chunks - b + cta_per - 1) / cta_per : 0;
+    auto issue = [&](size_t k) {
+      const size_t c = b + k * cta_per;
+      const int st = (int)(k % kStages);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])), "r"(kChunk) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sm + st * kChunk)), "l"(src + c * kChunk), "r"(kChunk), "r"(smem_u32(&bar[st])) : "memory");
+    };
+    for (; issued < mine && issued < kStages; ++issued) issue(issued);
+    for (; done < mine; ++done) {
+      const int st = (int)(done % kStages);
+      const unsigned par = (unsigned)((done / kStages) & 1);
+      asm volatile("{\n .reg .pred P;\n W: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra W;\n}" ::"r"(smem_u32(&bar[st])), "r"(par) : "memory");
+      const size_t c = b + done * cta_per;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + c * kChunk), "r"(smem_u32(sm + st * kChunk)), "r"(kChunk) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (issued < mine) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        issue(issued++);
+      }
+      (void)phase;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 int main(int argc, char** argv) {
   int N = 0;
   cudaGetDeviceCount(&N);
@@ -46,8 +89,12 @@ int main(int argc, char** argv) {
     cudaMemset(out[g], g + 1, per_pair * N);
     for (int h = 0; h < N; ++h) cudaStreamCreateWithFlags(&st[g][h], cudaStreamNonBlocking);
   }
-  const char* names[3] = {"pull(SM loads)", "push(SM stores)", "ce(peer memcpy)"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* names[4] = {"pull(SM loads)", "push(SM stores)", "ce(peer memcpy)", "pull(TMA bulk)"};
+  for (int g = 0; g < N; ++g) {
+    cudaSetDevice(g);
+    cudaFuncSetAttribute(a2a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384);
+  }
+  for (int mode = 0; mode < 4; ++mode) {
     for (int ctas : {148, 296, 592}) {
       if (mode == 2 && ctas != 148) continue;
       std::vector<cudaEvent_t> e0(N), e1(N);
@@ -80,6 +127,9 @@ int main(int argc, char** argv) {
             ++k;
           }
           if (mode < 2) a2a_kernel<<<(ctas / (N - 1)) * (N - 1), 512, 0, st[g][0]>>>(p, n16);
+          if (mode == 3) {  // (same direction as the SM pull: g reads h's slot)
+            a2a_tma_kernel<<<(ctas * 2 / (N - 1)) * (N - 1), 32, 4 * 16384, st[g][0]>>>(p, per_pair);
+          }
           if (mode == 2) {
             for (int h = 0; h < N; ++h) {
               if (h == g) continue;
