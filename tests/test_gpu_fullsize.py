@@ -189,6 +189,29 @@ def test_gae_long_rollouts_deterministic(O, dfx):
     assert_close_vec(outs[0][1][:T].cpu().numpy(), Rt[:T], "long gae ret")
 
 
+def test_gae_segment_cuts(O, dfx):
+    """The segment scan around its cut rule: rollouts of 60k-140k tokens (some above the 64k no-cut limit, so their
+    segments chain through published carries, some below), through a view of records 1..5 (its first token at an
+    arbitrary offset); bit-identical on a second run and within tolerance of the oracle."""
+    streams = ("mask", "value_tok", "token_reward")
+    sb = O.SynthBatch(17, 7, 2, O.token_dist("uniform", 60000, 60000, 140000), streams=streams)
+    db = dfx.PackedBatch.synthetic(17, 7, 2, dfx.TokenDist("uniform", 60000, 60000, 140000), streams=streams)
+    r0, r1 = 1, 6
+    v = db.view_records(r0, r1)
+    s0, s1 = int(sb.group_off[r0]), int(sb.group_off[r1])
+    cu = np.ascontiguousarray(sb.cu_seqlens[s0:s1 + 1])
+    ctx = dfx.StageContext(gae_gamma=0.995, gae_lambda=0.97)
+    dfx.fn_gae_advantage(dfx.NodeSpec("g"), v, ctx)
+    a1 = v.streams["advantage"][cu[0]:cu[-1]].clone()
+    r1_ = v.streams["returns"][cu[0]:cu[-1]].clone()
+    dfx.fn_gae_advantage(dfx.NodeSpec("g"), v, ctx)
+    assert torch.equal(a1, v.streams["advantage"][cu[0]:cu[-1]])
+    assert torch.equal(r1_, v.streams["returns"][cu[0]:cu[-1]])
+    A, Rt, _ = O.gae(cu, sb.token_reward, sb.value_tok, sb.mask, 0.995, 0.97)
+    assert_close_vec(a1.cpu().numpy(), A[cu[0]:cu[-1]], "segment-cut gae adv")
+    assert_close_vec(r1_.cpu().numpy(), Rt[cu[0]:cu[-1]], "segment-cut gae ret")
+
+
 def test_workspace_reuse_across_sizes(O, dfx):
     """One workspace reused by calls of different sizes: GAE after a larger span, and the loss with a
     loss-group count crossing a multiple of 32 and back, all still equal to the oracle."""
