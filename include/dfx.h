@@ -114,17 +114,18 @@ dfx_status dfx_ppo_advantage(const dfx_packed* b, double* adv_roll, dfx_stream s
  * computed in f64 inside the kernel, stored f32. Optionally writes the masked
  * whitening sums whiten[3] = {sum m*A, sum m*A^2, sum m} (device f64). */
 /* One reverse affine scan over the whole token line (the chain breaks at rollout
- * ends by itself): a prep kernel marks rollout ends in a token bitmap, a
- * single-pass decoupled look-back scan over 4096-token CTA tiles does the rest
- * (f32 inputs/outputs, deltas and recurrences in f64), and with whitening a
- * finish kernel reduces the per-tile sums in tile order. Outputs are
- * bit-identical run to run: the look-back composes a data-determined set of
- * tile records (checkpoint tiles every 32 publish carried inclusives).
- * Workspace (dfx_gae_workspace_bytes) must be zero-filled once at allocation;
- * the kernels keep it consistent across calls (epoch-tagged tile records, the
- * end bitmap cleared as it is consumed), so it can be reused -- by calls of
- * any span up to its capacity: its layout depends only on ws_bytes -- and
- * graph-captured. */
+ * ends by itself): a prep kernel marks rollout ends in a token bitmap and cuts
+ * the line into rollout-aligned segments (about one per resident CTA); a
+ * persistent CTA scans its segment right to left in 2048-token tiles through a
+ * TMA ring, the carry in a register (a segment that cuts a rollout longer than
+ * 64K tokens takes the value its right neighbour publishes); f32
+ * inputs/outputs, deltas and recurrences in f64; with whitening a finish kernel
+ * reduces the per-segment sums in segment order. Outputs are bit-identical run
+ * to run. Workspace (dfx_gae_workspace_bytes) must be zero-filled once at
+ * allocation; the kernels keep it consistent across calls (epoch-tagged
+ * records, the end bitmap cleared as it is consumed), so it can be reused --
+ * by calls of any span up to its capacity: its layout depends only on
+ * ws_bytes -- and graph-captured. */
 size_t dfx_gae_workspace_bytes(int64_t n_rollouts, int64_t token_span);
 dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, double gamma, double lam,
                    float* adv, float* ret, double* whiten, void* workspace, size_t ws_bytes, dfx_stream stream);
@@ -134,8 +135,10 @@ dfx_status dfx_gae(const dfx_packed* b, int64_t token_base, int64_t token_span, 
  * never goes to HBM (adv may be NULL; ret is written for the critic). Token-
  * mean aggregation of unwhitened advantages only (cfg->agg ==
  * DFX_AGG_TOKEN_MEAN, cfg->whiten == 0: whitening needs the global advantage
- * statistics first -- use dfx_gae then dfx_ppo_loss). Same numerics as
- * dfx_gae followed by dfx_ppo_loss with DFX_ADV_TOKEN, deterministic.
+ * statistics first -- use dfx_gae then dfx_ppo_loss). The scan is the
+ * 4096-token-tile decoupled look-back (its per-tile loss phase is hidden by five
+ * independent CTAs per SM); numerics as dfx_gae followed by dfx_ppo_loss with
+ * DFX_ADV_TOKEN, within f64 rounding, deterministic.
  * Workspace zero-filled once at allocation (as dfx_gae's). */
 typedef struct dfx_loss_cfg dfx_loss_cfg;
 typedef struct dfx_loss_out dfx_loss_out;
