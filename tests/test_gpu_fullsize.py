@@ -257,6 +257,23 @@ def test_multi_source_with_empty_source(dfx):
     np.testing.assert_allclose(got[:5], whole[:5], rtol=2e-6, atol=1e-9)
 
 
+def test_multi_source_api_with_one_source(O, dfx):
+    """dfx_ppo_loss_multi with a single source runs the multi-source kernel (its sources may be peer memory: no
+    L2 prefetch there): same counts as, and the oracle's loss within 1e-5 like, the single-batch kernel."""
+    sb = O.SynthBatch(12, 64, 8, O.token_dist("uniform", 0, 1, 3000))
+    b = dfx.PackedBatch.synthetic(12, 64, 8, dfx.TokenDist("uniform", 0, 1, 3000))
+    ctx = dfx.StageContext()
+    dfx.fn_group_advantage(dfx.NodeSpec("a"), b, ctx)
+    single = dfx.ppo_loss(b, ctx, adv_source="rollout")["out"].cpu().numpy()[0]
+    multi = dfx.ppo_loss_sources([b], ctx, loss_group_off=[0, b.n_rollouts])["out"].cpu().numpy()[0]
+    assert multi[5] == single[5] and multi[6] == single[6]
+    adv = O.grpo_advantage(sb.group_off, sb.reward, 1e-6)
+    ref, _ = O.ppo_loss(sb.cu_seqlens, sb.lp, sb.old_lp, sb.ref_lp, O.broadcast_advantage(sb.cu_seqlens, adv, sb.mask),
+                        sb.mask, O.loss_cfg())
+    _check_loss(single, ref, "single-batch kernel")
+    _check_loss(multi, ref, "multi-source kernel, one source")
+
+
 @pytest.mark.parametrize("kl", ["k3", "k1", "none"])
 def test_c3_fused_gae_loss_full_size(O, dfx, kl):
     """C3 (512 x 8192) through the fused GAE + loss pass (dfx_gae_ppo_loss): two runs give the same bits; returns and
