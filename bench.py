@@ -456,7 +456,10 @@ def run_c4(args):
     to_s, to_t = Layout(dp // 2, 2), Layout(dp, 1)
     stages = {"s": StoreStagePlan(Layout(dp, 1), to_s), "t": StoreStagePlan(to_s, to_t)}
     R = 1024 // world
-    batch = dfx.PackedBatch.synthetic(11, R, 16, dfx.TokenDist("constant", 1024), device=dev, first_id=rank * R,
+    # (DFX_C4_RAGGED=1, benchmarking only: U[1,2047] lengths, so exchanged runs start at arbitrary 16-byte phases)
+    dist_c4 = (dfx.TokenDist("uniform", 0, 1, 2047) if os.environ.get("DFX_C4_RAGGED") == "1"
+               else dfx.TokenDist("constant", 1024))
+    batch = dfx.PackedBatch.synthetic(11, R, 16, dist_c4, device=dev, first_id=rank * R,
                                       streams=("token_id", "lp", "old_lp", "ref_lp"))
     dfx.fn_group_advantage(dfx.NodeSpec("a"), batch, dfx.StageContext())
     local_p = [p for p in range(dp) if topo.gpu_of_worker[p] == rank]

@@ -200,12 +200,8 @@ __global__ void __launch_bounds__(256) copy_many_kernel(CopyMany c) {
     for (uint64_t i = threadIdx.x; i < n / 16; i += blockDim.x)
       reinterpret_cast<uint4*>(dst)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
     for (uint64_t i = (n / 16) * 16 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-  } else if ((a & 3u) == 0) {
-    for (uint64_t i = threadIdx.x; i < n / 4; i += blockDim.x)
-      reinterpret_cast<uint32_t*>(dst)[i] = __ldcs(reinterpret_cast<const uint32_t*>(src) + i);
-    for (uint64_t i = (n / 4) * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-  } else {
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {  // different 16-byte phases: 16-byte stores assembled from the aligned source vectors
+    dfx::copy_shift16<false>(dst, src, n, threadIdx.x, blockDim.x);
   }
 }
 }  // namespace

@@ -134,6 +134,49 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Copy n bytes src -> dst when the two are in different 16-byte phases: aligned 16-byte stores to dst, each
+// assembled (funnel shifts) from the two aligned 16-byte source vectors it straddles -- neighbouring threads read
+// the same lines, so the traffic stays ~1x -- and the unaligned ends byte by byte. Threads tid, tid + nthr, ...
+// NC: read-only non-coherent loads (peer memory over NVLink), else streaming loads.
+template <bool NC>
+__device__ __forceinline__ uint4 ld_v4_src(const uint8_t* p) {
+  uint4 r;
+  if (NC)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  else
+    r = __ldcs(reinterpret_cast<const uint4*>(p));
+  return r;
+}
+template <bool NC>
+__device__ __forceinline__ void copy_shift16(uint8_t* dst, const uint8_t* src, uint64_t n, uint32_t tid,
+                                             uint32_t nthr) {
+  const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst), a0 = (d0 + 15) & ~uintptr_t(15);
+  const uint64_t head = (uint64_t)min((uintptr_t)n, a0 - d0);
+  const uint64_t nu = (n - head) / 16, tail0 = head + 16 * nu;
+  for (uint64_t j = tid; j < head; j += nthr) dst[j] = src[j];
+  for (uint64_t j = tail0 + tid; j < n; j += nthr) dst[j] = src[j];
+  const uintptr_t s1 = reinterpret_cast<uintptr_t>(src + head);  // the source of the first aligned unit
+  const uint8_t* sv = reinterpret_cast<const uint8_t*>(s1 & ~uintptr_t(15));
+  const uint32_t ph = (uint32_t)(s1 & 15u), q = ph >> 2, sh = (ph & 3u) * 8u;
+  const uintptr_t send = reinterpret_cast<uintptr_t>(src + n);
+  for (uint64_t u = tid; u < nu; u += nthr) {
+    const uint4 va = ld_v4_src<NC>(sv + 16 * u);
+    uint4 vb = make_uint4(0u, 0u, 0u, 0u);  // (only a unit that straddles two source vectors needs the second)
+    if (ph != 0 && reinterpret_cast<uintptr_t>(sv + 16 * u + 16) < send) vb = ld_v4_src<NC>(sv + 16 * u + 16);
+    const uint32_t w[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // source bytes ph .. ph + 15 of the 32: words q + k and q + k + 1, >> sh bits
+      const uint32_t lo = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
+      const uint32_t hi = q == 0 ? w[k + 1] : q == 1 ? w[k + 2] : q == 2 ? w[k + 3] : w[k + 4];
+      o[k] = __funnelshift_r(lo, hi, sh);
+    }
+    reinterpret_cast<uint4*>(dst + head)[u] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // ---- per-token loss math shared by the loss kernels (loss.cu) and the fused GAE + loss scan (gae.cu) ---------
 // k3 = e^x - x - 1 (x = ref - lp) by its Taylor series for |x| < 1/8 (truncation < 1.2e-8 relative); callers
 // fall back to expm1f(x) - x, which has no cancellation, for larger |x|.

@@ -340,7 +340,8 @@ __global__ void __launch_bounds__(512) peer_pull_kernel(const PullList c) {
       for (; i < nv; i += step) reinterpret_cast<uint4*>(dst)[i] = ld_nc_v4(src + 16 * i);
       for (uint64_t j = nv * 16 + threadIdx.x; j < n; j += step) dst[j] = src[j];
     } else {
-      for (uint64_t j = threadIdx.x; j < n; j += blockDim.x) dst[j] = src[j];
+      // source and destination in different 16-byte phases (runs start at arbitrary token offsets)
+      copy_shift16<true>(dst, src, n, threadIdx.x, blockDim.x);
     }
   }
 }
