@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(256) copy_sm_kernel(uint8_t* __restrict__ dst,
   } else if (width == 4) {
     for (uint64_t i = i0; i < n / 4; i += step) reinterpret_cast<uint32_t*>(dst)[i] = __ldcs(reinterpret_cast<const uint32_t*>(src) + i);
     for (uint64_t i = (n / 4) * 4 + i0; i < n; i += step) dst[i] = src[i];
-  } else {
-    for (uint64_t i = i0; i < n; i += step) dst[i] = src[i];
+  } else {  // different 16-byte phases: 16-byte stores assembled from the aligned source vectors
+    dfx::copy_shift16<false>(dst, src, n, (uint32_t)i0, (uint32_t)step);
   }
 }
 // record metadata of a view of records [r0, r1): group_off rebased to its first rollout, roll_group to r0
@@ -243,7 +243,7 @@ dfx_status dfx_view_meta(const int32_t* group_off, const int32_t* roll_group, in
 dfx_status dfx_copy_sm(void* dst, const void* src, size_t bytes, dfx_stream stream) {
   if (bytes == 0) return DFX_OK;
   const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
-  const int width = (a & 15u) == 0 ? 16 : (a & 3u) == 0 ? 4 : 1;
+  const int width = (a & 15u) == 0 ? 16 : 1;  // (1: copy_shift16)
   const uint64_t units = bytes / uint64_t(width) + 1;
   const unsigned grid = (unsigned)std::min<uint64_t>((units + 255) / 256, 148ull * 8);
   copy_sm_kernel<<<grid, 256, 0, stream>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes, width);

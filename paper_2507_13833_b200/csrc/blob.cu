@@ -263,15 +263,15 @@ struct UnblobParams {
   double* ch[kBlobMaxCh];
 };
 
-// dst aligned to 4 bytes at its start (element streams are), src any alignment
+// 4-byte-aligned dst: 32-bit stores assembled by funnel shifts from aligned source words; else copy_shift16
 __device__ __forceinline__ void block_gather(uint8_t* dst, const uint8_t* src, uint64_t n) {
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
   const uint32_t sh = uint32_t(sa & 3u) * 8u;
   const uint64_t nw = n / 4;
   uint32_t* dw = reinterpret_cast<uint32_t*>(dst);
-  if (reinterpret_cast<uintptr_t>(dst) & 3u) {
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  if (reinterpret_cast<uintptr_t>(dst) & 3u) {  // (byte streams at an odd token offset)
+    copy_shift16<false>(dst, src, n, threadIdx.x, blockDim.x);
     return;
   }
   for (uint64_t w = threadIdx.x; w < nw; w += blockDim.x)
