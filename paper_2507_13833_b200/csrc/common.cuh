@@ -135,8 +135,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // Copy n bytes src -> dst when the two are in different 16-byte phases: aligned 16-byte stores to dst, each
-// assembled (funnel shifts) from the two aligned 16-byte source vectors it straddles -- neighbouring threads read
-// the same lines, so the traffic stays ~1x -- and the unaligned ends byte by byte. Threads tid, tid + nthr, ...
+// assembled (funnel shifts) from the two aligned 16-byte source vectors it straddles, and the unaligned ends byte by
+// byte. Threads tid, tid + nthr, ... with nthr a multiple of 32 and whole warps calling (warp shuffles).
 // NC: read-only non-coherent loads (peer memory over NVLink), else streaming loads.
 template <bool NC>
 __device__ __forceinline__ uint4 ld_v4_src(const uint8_t* p) {
@@ -161,19 +161,44 @@ __device__ __forceinline__ void copy_shift16(uint8_t* dst, const uint8_t* src, u
   const uint8_t* sv = reinterpret_cast<const uint8_t*>(s1 & ~uintptr_t(15));
   const uint32_t ph = (uint32_t)(s1 & 15u), q = ph >> 2, sh = (ph & 3u) * 8u;
   const uintptr_t send = reinterpret_cast<uintptr_t>(src + n);
-  for (uint64_t u = tid; u < nu; u += nthr) {
-    const uint4 va = ld_v4_src<NC>(sv + 16 * u);
-    uint4 vb = make_uint4(0u, 0u, 0u, 0u);  // (only a unit that straddles two source vectors needs the second)
-    if (ph != 0 && reinterpret_cast<uintptr_t>(sv + 16 * u + 16) < send) vb = ld_v4_src<NC>(sv + 16 * u + 16);
-    const uint32_t w[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-    uint32_t o[4];
+  // warp-uniform rounds of two units per lane: lane l takes units base + l and base + nthr + l, and gets the vector
+  // after each from lane l + 1 by a shuffle, so every source vector is read once (lane 31 reads its second vectors
+  // itself); both units' loads are in flight together
+  const uint32_t lane = tid & 31u;
+  for (uint64_t base = tid - lane; base < nu; base += 2 * (uint64_t)nthr) {
+    uint4 va[2];
+    bool in[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // source bytes ph .. ph + 15 of the 32: words q + k and q + k + 1, >> sh bits
-      const uint32_t lo = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
-      const uint32_t hi = q == 0 ? w[k + 1] : q == 1 ? w[k + 2] : q == 2 ? w[k + 3] : w[k + 4];
-      o[k] = __funnelshift_r(lo, hi, sh);
+    for (int r = 0; r < 2; ++r) {
+      const uint64_t u = base + (uint64_t)r * nthr + lane;
+      in[r] = u < nu;
+      va[r] = make_uint4(0u, 0u, 0u, 0u);
+      if (in[r]) va[r] = ld_v4_src<NC>(sv + 16 * u);
     }
-    reinterpret_cast<uint4*>(dst + head)[u] = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint64_t u = base + (uint64_t)r * nthr + lane;
+      uint4 vb;
+      vb.x = __shfl_down_sync(0xffffffffu, va[r].x, 1);
+      vb.y = __shfl_down_sync(0xffffffffu, va[r].y, 1);
+      vb.z = __shfl_down_sync(0xffffffffu, va[r].z, 1);
+      vb.w = __shfl_down_sync(0xffffffffu, va[r].w, 1);
+      if (lane == 31 || u + 1 >= nu) {  // (the second vector is only needed when the unit straddles two)
+        vb = make_uint4(0u, 0u, 0u, 0u);
+        if (in[r] && ph != 0 && reinterpret_cast<uintptr_t>(sv + 16 * u + 16) < send)
+          vb = ld_v4_src<NC>(sv + 16 * u + 16);
+      }
+      if (!in[r]) continue;
+      const uint32_t w[8] = {va[r].x, va[r].y, va[r].z, va[r].w, vb.x, vb.y, vb.z, vb.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // source bytes ph .. ph + 15 of the 32: words q + k and q + k + 1, >> sh bits
+        const uint32_t lo = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
+        const uint32_t hi = q == 0 ? w[k + 1] : q == 1 ? w[k + 2] : q == 2 ? w[k + 3] : w[k + 4];
+        o[k] = __funnelshift_r(lo, hi, sh);
+      }
+      reinterpret_cast<uint4*>(dst + head)[u] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
