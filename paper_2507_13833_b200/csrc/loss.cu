@@ -32,9 +32,6 @@
 #ifndef DFX_TOKEN_MINB
 #define DFX_TOKEN_MINB 2
 #endif
-#ifndef DFX_TOKEN_DB
-#define DFX_TOKEN_DB 0
-#endif
 #ifndef DFX_TOKEN_UNROLL
 #define DFX_TOKEN_UNROLL 2
 #endif
@@ -489,10 +486,20 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
   int k = MULTI ? (int)(gwarp % p.n_src) : 0;
   uint32_t live = (1u << p.n_src) - 1u;
 
-  for (;;) {
-    unsigned long long uu = 0;
-    if (lane == 0) uu = atomicAdd(next + k, 1ull);
-    const int64_t ul = (int64_t)__shfl_sync(kFull, uu, 0);
+  // at most one slot per warp (e.g. C3: 2048 slots, 2368 resident warps): warp w takes slot w, no ticket atomics
+  // (claiming would balance nothing and costs two dependent atomic round trips per warp). Per-token-advantage path
+  // only: in the 80-register per-rollout kernels any extra live state spills
+  const bool one_each = ADV == DFX_ADV_TOKEN && !MULTI && p.n_slots <= nwarps;
+  for (bool first = true;; first = false) {
+    int64_t ul;
+    if (one_each) {
+      if (!first) break;
+      ul = gwarp;
+    } else {
+      unsigned long long uu = 0;
+      if (lane == 0) uu = atomicAdd(next + k, 1ull);
+      ul = (int64_t)__shfl_sync(kFull, uu, 0);
+    }
     const int64_t kend = MULTI ? (k + 1 < p.n_src ? p.src[k + 1].slot0 : p.n_slots) - p.src[k].slot0 : p.n_slots;
     if (ul >= kend) {
       if (!MULTI) break;
@@ -559,10 +566,9 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
                   (uint32_t)((reinterpret_cast<uintptr_t>(mk0) + 4u * (uint32_t)nvec - m0 + 15u) & ~uintptr_t(15)));
     }
 #endif
-    // one round: kUnroll vectors per lane, lane-strided. load_round issues the round's stream loads (predicated)
-    // and the L2 prefetch DFX_LOSS_PFR rounds after it; use_round folds the loaded vectors into the slot's sums
-    auto load_round = [&](int32_t ib, float4(&lv)[kUnroll], float4(&ov)[kUnroll], float4(&rv)[kUnroll],
-                          float4(&av)[kUnroll], uint32_t(&mk)[kUnroll]) {
+    for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
+      float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
+      uint32_t mk[kUnroll];
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j) {
         const int32_t i = ib + 32 * j;
@@ -596,9 +602,6 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
         }
 #endif
       }
-    };
-    auto use_round = [&](int32_t ib, const float4(&lv)[kUnroll], const float4(&ov)[kUnroll],
-                         const float4(&rv)[kUnroll], const float4(&av)[kUnroll], const uint32_t(&mk)[kUnroll]) {
       TokAcc acc{0.f, 0.f, 0.f, 0u, 0u};
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j) {
@@ -623,33 +626,6 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
       dakl += acc.akl;
       nclip += acc.clip;
       nmask += acc.n;
-    };
-#if DFX_TOKEN_DB
-    if constexpr (ADV == DFX_ADV_TOKEN && !MULTI) {
-      // register double buffer (per-token-advantage path): the next round's loads are issued before this round's
-      // math, so the math of one round overlaps the memory latency of the next. Two buffers used in turn (no
-      // register copies, which would wait for the loads in flight)
-      float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll], lv2[kUnroll], ov2[kUnroll], rv2[kUnroll],
-          av2[kUnroll];
-      uint32_t mk[kUnroll], mk2[kUnroll];
-      constexpr int32_t kStep = 32 * kUnroll;
-      load_round(lane, lv, ov, rv, av, mk);
-      for (int32_t ib = lane; ib < nvec; ib += 2 * kStep) {
-        load_round(ib + kStep, lv2, ov2, rv2, av2, mk2);
-        use_round(ib, lv, ov, rv, av, mk);
-        if (ib + kStep >= nvec) break;
-        load_round(ib + 2 * kStep, lv, ov, rv, av, mk);
-        use_round(ib + kStep, lv2, ov2, rv2, av2, mk2);
-      }
-    } else
-#endif
-    {
-      for (int32_t ib = lane; ib < nvec; ib += 32 * kUnroll) {
-        float4 lv[kUnroll], ov[kUnroll], rv[kUnroll], av[kUnroll];
-        uint32_t mk[kUnroll];
-        load_round(ib, lv, ov, rv, av, mk);
-        use_round(ib, lv, ov, rv, av, mk);
-      }
     }
     dpg = warp_sum(dpg);
     dkl = warp_sum(dkl);
@@ -665,7 +641,7 @@ __global__ void __launch_bounds__(256, MINB) loss_slots_kernel(LossParams p) {
     }
   }
   // the last warp out restores the tickets for the next launch
-  if (lane == 0) {
+  if (!one_each && lane == 0) {
     __threadfence();
     const unsigned long long done = atomicAdd(next + kMaxLossSrc, 1ull);
     if (done == (unsigned long long)nwarps - 1) {
