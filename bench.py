@@ -148,9 +148,10 @@ def measured_peak_hbm():
 
 def ncu_traffic():
     """dram bytes per launch of the dominant kernel from the newest committed ncu --set full capture
-    (profiles/*loss_slots*.json, written by tools/ncu_summary.py from a capture of the same C2 step)."""
+    (profiles/*loss_slots*.json, written by tools/ncu_summary.py from a capture of the same C2 step). Newest by
+    the round-tagged file name (r01s3_ < r02h_ < r02i_ ...): a fresh checkout gives every file the same mtime."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*loss_slots*.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*loss_slots*.json")), key=os.path.basename)
     for p in reversed(files):
         try:
             with open(p) as f:
